@@ -78,3 +78,57 @@ def dual_certificate(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1e-7, t
         out["ok"] = False
         out["reasons"].append(f"duality gap {UB - LB}")
     return out
+
+
+def dual_certificate_batch(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1e-7, tol_z=1e-7,
+                           tol_gap=1e-6):
+    """dual_certificate over a batch of frames ([F, n] / [F, m] arrays), vectorised with numpy
+    (same three checks, same tolerances).  Returns a dict of per-frame arrays incl. ok."""
+    gamma = np.asarray(gamma, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    masks = np.asarray(masks).astype(np.int64) & 0xFFFF
+    Fn, n = u.shape
+    m = code.m
+    deg = np.diff(code.row_ptr).astype(np.int64)
+    dc = int(deg.max())
+    Nb = np.zeros((m, dc), dtype=np.int64)
+    valid = np.arange(dc)[None, :] < deg[:, None]
+    for j in range(m):
+        Nb[j, :deg[j]] = code.N(j)
+    un = u[:, Nb]                                         # [F, m, dc]
+    # (i) Alg. 2 on every check
+    S = (un > 0.5) & valid
+    cntS = S.sum(axis=2)
+    dist = np.where(valid, np.abs(un - 0.5), np.inf)
+    istar = np.argmin(dist, axis=2)                       # first minimum = lowest position
+    toggle = (cntS % 2 == 0)[..., None] & (np.arange(dc)[None, None, :] == istar[..., None])
+    V = S ^ toggle
+    lhs = np.where(valid, np.where(V, 1.0 - un, un), 0.0).sum(axis=2)
+    min_lhs = lhs.min(axis=1)
+    ok = min_lhs >= 1.0 - tol_cut
+    ok &= np.all((u >= -tol_box) & (u <= 1.0 + tol_box), axis=1)
+    # (ii) dual feasibility on the final pool LP
+    flip = gamma < 0
+    c = np.abs(gamma)
+    cn = c.max(axis=1)
+    present = ((masks >> 15) & 1).astype(bool)            # [F, m]
+    inV = ((masks[..., None] >> np.arange(dc)[None, None, :]) & 1).astype(bool) & valid
+    a = np.where(inV, 1.0, -1.0)
+    fl = flip[:, Nb]                                      # [F, m, dc]
+    coef = np.where(valid, a * np.where(fl, -1.0, 1.0), 0.0)
+    yp = np.where(present, y, 0.0)
+    z = c.copy()
+    contrib = (coef * yp[..., None])                      # [F, m, dc]
+    flat = (np.arange(Fn)[:, None, None] * n + Nb[None, :, :])
+    np.subtract.at(z.reshape(-1), flat[:, valid].reshape(-1), contrib[:, valid].reshape(-1))
+    b = inV.sum(axis=2) - 1.0 - np.where(valid & fl, a, 0.0).sum(axis=2)
+    ok &= np.all(~present | (y <= tol_z), axis=1)
+    ok &= z.min(axis=1) >= -tol_z * (1.0 + cn)
+    x = np.where(flip, 1.0 - u, u)
+    UB = (c * x).sum(axis=1)
+    LB = (np.where(present, b * y, 0.0)).sum(axis=1) + np.minimum(0.0, z).sum(axis=1) \
+        + np.where(present, np.minimum(0.0, -y) * deg[None, :], 0.0).sum(axis=1)
+    gap = UB - LB
+    ok &= gap <= tol_gap * (1.0 + np.abs(UB))
+    return dict(ok=ok, min_lhs=min_lhs, gap=gap, UB=UB, LB=LB)

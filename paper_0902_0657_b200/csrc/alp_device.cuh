@@ -1,0 +1,773 @@
+// alp_device.cuh — warp-per-frame device building blocks of libalp (sm_100a).
+//
+// One warp owns one frame (or one isolated step system) at a time; every step of the
+// method runs inside that warp with lane-strided loops, warp-shuffle reductions and
+// __syncwarp barriers.  Per-frame vectors live in a per-warp "slot" of global memory
+// (frame-major, contiguous, reused frame after frame so the live set stays L2-resident);
+// the latency-critical sequential parts (column sort, Alg. 7 peel, level build) and the
+// gathered PCG vectors live in the warp's shared-memory window, whose phases alias.
+// Citations: PAPER.md line numbers (P:n) with section / algorithm / equation label.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace alp {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint16_t PRESENT = 0x8000u;
+constexpr uint16_t NONE16 = 0xffffu;
+constexpr int DCMAX = 15;  // d_c <= 15 (mask bits 0..14)
+constexpr int DVMAX = 4;   // d_v <= 4  (sgnV packing: 4 present bits + 4 sign bits)
+constexpr int RF = 4;      // forward-record ints: head + up to d_v - 1 deps
+
+// frame status bits (include/alp.h alp_frame_status)
+constexpr int ST_ALP_MAXITER = 1, ST_IPM_MAXITER = 2, ST_PCG_MAXITER = 4, ST_PCG_BREAKDOWN = 8,
+              ST_NUMERIC = 16;
+
+struct Params {
+  int variant, precond;
+  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, tau_viol, tau_act, tau_cert;
+  int alp_max_iter, ipm_max_iter, pcg_max_iter;
+};
+
+// Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
+struct DCode {
+  int n, m, dc, dv, Q, QP2, W, RB;        // Q = n + m columns, QP2 = pow2 >= Q, W = bitmap words
+  const int* __restrict__ chk_var;        // [m][dc] sorted variables of each check, -1 padded
+  const uint8_t* __restrict__ chk_deg;    // [m]
+  const int* __restrict__ var_chk;        // [n][dv] checks of each variable, -1 padded
+  const uint8_t* __restrict__ var_slot;   // [n][dv] position t of the variable in N(check)
+  const uint8_t* __restrict__ var_deg;    // [n]
+};
+
+// Byte offsets inside one warp's global slot and shared-memory window (host-computed).
+struct Layout {
+  long long slot_bytes;
+  long long g_x, g_z, g_d2, g_v, g_y, g_dy, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
+      g_offF, g_sgnC, g_mask, g_sgnV, g_flip;
+  int smem_bytes;
+  int s_keys;                                                                  // sort phase
+  int s_order, s_rank, s_cnt, s_xr, s_bm, s_pos, s_pcol, s_prow, s_lvB, s_lvF;  // peel phase
+  int s_poc, s_hist, s_cur;                                                    // post-peel
+  int s_h, s_r, s_f, s_z, s_t;                                                 // PCG phase
+};
+
+// ------------------------------------------------------------------ warp reductions
+// xor-butterflies: every lane ends with the bit-identical result (commutative adds), so
+// decisions taken on reduced values are warp-uniform.
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ double wmin(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ int wsumi(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ int wmaxi(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// Per-frame working set: pointers into the warp's global slot and shared window.
+struct Frame {
+  const DCode* C;
+  const Layout* L;
+  int lane;
+  char* sm;
+  double *x, *z, *d2, *v, *y, *dy, *l, *w, *u, *b, *dinvF;
+  int *recB, *recF, *offB, *offF;
+  uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
+  uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
+  uint8_t* sgnV;   // [n]: bit k <-> k-th check of the variable present; bit 4+k <-> coef -1
+  uint8_t* flip;   // [n]: 1 <-> gamma_i < 0 (x_i = 1 - u_i, §IV-B)
+  template <class T>
+  __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(sm + off); }
+};
+
+__device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layout* L, char* slot,
+                                           char* sm, int lane) {
+  F.C = C;
+  F.L = L;
+  F.lane = lane;
+  F.sm = sm;
+  F.x = (double*)(slot + L->g_x);
+  F.z = (double*)(slot + L->g_z);
+  F.d2 = (double*)(slot + L->g_d2);
+  F.v = (double*)(slot + L->g_v);
+  F.y = (double*)(slot + L->g_y);
+  F.dy = (double*)(slot + L->g_dy);
+  F.l = (double*)(slot + L->g_l);
+  F.w = (double*)(slot + L->g_w);
+  F.u = (double*)(slot + L->g_u);
+  F.b = (double*)(slot + L->g_b);
+  F.dinvF = (double*)(slot + L->g_dinvF);
+  F.recB = (int*)(slot + L->g_recB);
+  F.recF = (int*)(slot + L->g_recF);
+  F.offB = (int*)(slot + L->g_offB);
+  F.offF = (int*)(slot + L->g_offF);
+  F.sgnC = (uint16_t*)(slot + L->g_sgnC);
+  F.mask = (uint16_t*)(slot + L->g_mask);
+  F.sgnV = (uint8_t*)(slot + L->g_sgnV);
+  F.flip = (uint8_t*)(slot + L->g_flip);
+}
+
+__device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
+  return __ldg(C.chk_var + j * C.dc + t);
+}
+__device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
+  return __ldg(C.var_chk + i * C.dv + k);
+}
+
+// =====================================================================================
+// Sign tables of the augmented constraint matrix (§IV-B, eq.`MALP matrix form`).
+// Check j with cut V, variable i = N(j)[t]: A_ji = a s, a = +1 on V else -1 (eq.`constraints`
+// P:107-110), s = -1 if gamma_i < 0.  A_ji < 0 <=> (i in V) == flipped.
+// b_j = |V| - 1 - sum_{i in N(j), flipped} a_ji.  Returns p (rows), n_act (standard columns
+// with >= 1 row), ||b||_inf.
+// =====================================================================================
+__device__ void build_signs(const Frame& F, bool want_b, int& p_out, int& nact_out,
+                            double& bmax_out) {
+  const DCode& C = *F.C;
+  int p = 0;
+  double bmax = 0.0;
+  for (int j = F.lane; j < C.m; j += 32) {
+    uint16_t mk = F.mask[j];
+    uint16_t s = 0;
+    if (mk & PRESENT) {
+      int deg = C.chk_deg[j];
+      int nflipV = 0, nflipNotV = 0;
+      for (int t = 0; t < deg; ++t) {
+        int i = chk_nb(C, j, t);
+        int inV = (mk >> t) & 1, fl = F.flip[i];
+        if (inV == fl) s |= (uint16_t)(1u << t);
+        if (fl) {
+          if (inV) ++nflipV;
+          else ++nflipNotV;
+        }
+      }
+      s |= PRESENT;
+      ++p;
+      if (want_b) {
+        double bj = (double)(__popc(mk & 0x7fff) - 1) - (double)(nflipV - nflipNotV);
+        F.b[j] = bj;
+        bmax = fmax(bmax, fabs(bj));
+      }
+    }
+    F.sgnC[j] = s;
+  }
+  __syncwarp();
+  int nact = 0;
+  for (int i = F.lane; i < C.n; i += 32) {
+    int dv = C.var_deg[i];
+    uint8_t s = 0;
+    for (int k = 0; k < dv; ++k) {
+      int j = var_ck(C, i, k);
+      int t = C.var_slot[i * C.dv + k];
+      uint16_t sc = F.sgnC[j];
+      if (sc & PRESENT) {
+        s |= (uint8_t)(1u << k);
+        if ((sc >> t) & 1) s |= (uint8_t)(1u << (4 + k));
+      }
+    }
+    F.sgnV[i] = s;
+    nact += (s & 0xf) ? 1 : 0;
+  }
+  p_out = wsumi(p);
+  nact_out = wsumi(nact);
+  bmax_out = wmax(bmax);
+  __syncwarp();
+}
+
+// =====================================================================================
+// Alg. 2 + MALP-A / MALP-B pool update (Alg. 3 lines 5-11 P:224-235).
+// Every check reads the same u^{k-1}.  A present cut that is active (slack <= tau_act,
+// C-4) excludes its check (line 6, Cor. 2 P:208-213); MALP-B drops inactive cuts first.
+// S = {u_i > 1/2}; |S| even -> toggle i* = argmin |u_i - 1/2| (lowest position on ties,
+// C-2); violated iff lhs < 1 - tau_viol (C-3) -> the check's cut is replaced (line 8-9).
+// Returns warp-uniform "changed".
+// =====================================================================================
+__device__ bool cut_search(const Frame& F, const Params& P) {
+  const DCode& C = *F.C;
+  bool changed = false;
+  for (int j = F.lane; j < C.m; j += 32) {
+    int deg = C.chk_deg[j];
+    double uu[DCMAX];
+#pragma unroll
+    for (int t = 0; t < DCMAX; ++t) uu[t] = (t < deg) ? F.u[chk_nb(C, j, t)] : 0.0;
+    uint16_t mk = F.mask[j];
+    if (mk & PRESENT) {
+      double lhs = 0.0;
+#pragma unroll
+      for (int t = 0; t < DCMAX; ++t)
+        if (t < deg) lhs += ((mk >> t) & 1) ? (1.0 - uu[t]) : uu[t];
+      if (lhs - 1.0 <= P.tau_act) continue;   // active cut: check skipped
+      if (P.variant == 1) F.mask[j] = 0;       // MALP-B: remove the inactive cut
+    }
+    int S = 0, cnt = 0, istar = 0;
+    double best = 4.0;
+#pragma unroll
+    for (int t = 0; t < DCMAX; ++t) {
+      if (t < deg) {
+        if (uu[t] > 0.5) {
+          S |= 1 << t;
+          ++cnt;
+        }
+        double dd = fabs(uu[t] - 0.5);
+        if (dd < best) {
+          best = dd;
+          istar = t;
+        }
+      }
+    }
+    int V = (cnt & 1) ? S : (S ^ (1 << istar));
+    double lhs = 0.0;
+#pragma unroll
+    for (int t = 0; t < DCMAX; ++t)
+      if (t < deg) lhs += ((V >> t) & 1) ? (1.0 - uu[t]) : uu[t];
+    if (lhs < 1.0 - P.tau_viol) {
+      F.mask[j] = (uint16_t)(V | PRESENT);
+      changed = true;
+    }
+  }
+  __syncwarp();
+  return __any_sync(FULL, changed);
+}
+
+// =====================================================================================
+// Preconditioner build, part 1: rank the columns by weight (Alg. 7 needs "the maximum
+// weight d_i" among DEG1; weight d^2 = x/z gives the same order, C-10).
+// Packed 64-bit keys (~float(d^2) bits << 32 | column) sorted ascending by a warp bitonic
+// sort in shared memory = descending float weight, ascending column; runs of equal float
+// keys are then re-ordered by the exact fp64 weight (ties -> lower column).  Columns
+// without a present row (degree 0 in the extended Tanner graph) sort last.
+// =====================================================================================
+__device__ void sort_columns(const Frame& F) {
+  const DCode& C = *F.C;
+  uint64_t* keys = F.S<uint64_t>(F.L->s_keys);
+  for (int c = F.lane; c < C.QP2; c += 32) {
+    uint64_t k = ~0ull;
+    if (c < C.Q) {
+      bool valid = (c < C.n) ? ((F.sgnV[c] & 0xf) != 0) : ((F.sgnC[c - C.n] & PRESENT) != 0);
+      if (valid) {
+        float f = __double2float_rn(F.d2[c]);  // monotone non-decreasing map
+        uint32_t fb = __float_as_uint(f) & 0x7fffffffu;
+        k = ((uint64_t)(~fb) << 32) | (uint32_t)c;
+      }
+    }
+    keys[c] = k;
+  }
+  __syncwarp();
+  const int N = C.QP2;
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = F.lane; t < (N >> 1); t += 32) {
+        int lo = 2 * j * (t / j) + (t % j);
+        int hi = lo + j;
+        bool up = ((lo & k) == 0);
+        uint64_t a = keys[lo], b = keys[hi];
+        if ((a > b) == up) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  bool tie = false;
+  for (int r = F.lane; r + 1 < C.Q; r += 32) {
+    uint64_t a = keys[r], b = keys[r + 1];
+    if (a != ~0ull && b != ~0ull && (a >> 32) == (b >> 32)) tie = true;
+  }
+  if (__any_sync(FULL, tie)) {
+    if (F.lane == 0) {
+      int r = 0;
+      while (r + 1 < C.Q && keys[r] != ~0ull) {
+        uint64_t hi32 = keys[r] >> 32;
+        int e = r + 1;
+        while (e < C.Q && keys[e] != ~0ull && (keys[e] >> 32) == hi32) ++e;
+        for (int a = r + 1; a < e; ++a) {  // insertion sort by (d2 desc, column asc)
+          uint64_t ka = keys[a];
+          int ca = (int)(ka & 0xffffffffu);
+          double wa = F.d2[ca];
+          int b = a - 1;
+          while (b >= r) {
+            int cb = (int)(keys[b] & 0xffffffffu);
+            double wb = F.d2[cb];
+            if (!((wa > wb) || (wa == wb && ca < cb))) break;
+            keys[b + 1] = keys[b];
+            --b;
+          }
+          keys[b + 1] = ka;
+        }
+        r = e;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Part 2: Alg. 7.  DEG1 (line 4) is a bitmap over ranks; line 6 = first set bit.
+// For each column: number of live rows and XOR of their ids (the unique live row of a
+// degree-1 column).  Pick k records pos[R] = k, pcol[R] = c, prow[k] = R (line 7) and
+// zeroes row R (line 8), updating degrees and DEG1 (line 9).
+__device__ void peel_columnwise(const Frame& F, int p) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  uint64_t* keys = F.S<uint64_t>(L.s_keys);
+  uint16_t* order = F.S<uint16_t>(L.s_order);
+  uint16_t* rank = F.S<uint16_t>(L.s_rank);
+  uint8_t* cnt = F.S<uint8_t>(L.s_cnt);
+  uint16_t* xr = F.S<uint16_t>(L.s_xr);
+  unsigned long long* bm = F.S<unsigned long long>(L.s_bm);
+  uint16_t* pos = F.S<uint16_t>(L.s_pos);
+  uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
+  uint16_t* prow = F.S<uint16_t>(L.s_prow);
+  // in-place extraction of the sorted order (chunked: a lane never overwrites an unread key)
+  for (int base = 0; base < C.Q; base += 32) {
+    int r = base + F.lane;
+    uint16_t o = NONE16;
+    if (r < C.Q) {
+      uint64_t k = keys[r];
+      o = (k == ~0ull) ? NONE16 : (uint16_t)(k & 0xffffu);
+    }
+    __syncwarp();
+    if (r < C.Q) order[r] = o;
+    __syncwarp();
+  }
+  for (int c = F.lane; c < C.Q; c += 32) rank[c] = NONE16;
+  for (int w = F.lane; w < C.W; w += 32) bm[w] = 0ull;
+  __syncwarp();
+  for (int r = F.lane; r < C.Q; r += 32) {
+    uint16_t c = order[r];
+    if (c != NONE16) rank[c] = (uint16_t)r;
+  }
+  __syncwarp();
+  for (int c = F.lane; c < C.Q; c += 32) {
+    int cn = 0, x = 0;
+    if (c < C.n) {
+      uint8_t s = F.sgnV[c];
+      int dv = C.var_deg[c];
+      for (int k = 0; k < dv; ++k)
+        if ((s >> k) & 1) {
+          ++cn;
+          x ^= var_ck(C, c, k);
+        }
+    } else if (F.sgnC[c - C.n] & PRESENT) {
+      cn = 1;
+      x = c - C.n;
+    }
+    cnt[c] = (uint8_t)cn;
+    xr[c] = (uint16_t)x;
+    if (cn == 1) {
+      int r = rank[c];
+      atomicOr(&bm[r >> 6], 1ull << (r & 63));
+    }
+  }
+  __syncwarp();
+  for (int k = 0; k < p; ++k) {
+    int r = 0;
+    for (int base = 0; base < C.W; base += 32) {
+      unsigned long long wd = (base + F.lane < C.W) ? bm[base + F.lane] : 0ull;
+      unsigned bal = __ballot_sync(FULL, wd != 0ull);
+      if (bal) {
+        int src = __ffs(bal) - 1;
+        unsigned long long w0 = __shfl_sync(FULL, wd, src);
+        r = (base + src) * 64 + (__ffsll((long long)w0) - 1);
+        break;
+      }
+    }
+    int c = order[r];
+    int R = xr[c];
+    if (F.lane == 0) {
+      pos[R] = (uint16_t)k;
+      pcol[R] = (uint16_t)c;
+      prow[k] = (uint16_t)R;
+    }
+    int deg = C.chk_deg[R];
+    if (F.lane <= deg) {
+      int cc = (F.lane < deg) ? chk_nb(C, R, F.lane) : (C.n + R);
+      int nc = (int)cnt[cc] - 1;
+      cnt[cc] = (uint8_t)nc;
+      xr[cc] = (uint16_t)(xr[cc] ^ R);
+      int rr = rank[cc];
+      if (nc == 1) atomicOr(&bm[rr >> 6], 1ull << (rr & 63));
+      else if (nc == 0) atomicAnd(&bm[rr >> 6], ~(1ull << (rr & 63)));
+    }
+    __syncwarp();
+  }
+}
+
+// Sweep dependencies of the pivot on row R (A_M is upper triangular in pick order):
+//  back  (A_M f = r):   the other pivot columns of row R -> their pivot rows (picked later)
+//  fwd   (A_M^T z = g): the other present rows of column C_k (killed earlier)
+// Encoded row | (coefficient < 0) << 31.
+__device__ __forceinline__ int back_deps(const Frame& F, int R, int* deps) {
+  const DCode& C = *F.C;
+  const uint16_t* poc = F.S<uint16_t>(F.L->s_poc);
+  int deg = C.chk_deg[R];
+  uint16_t s = F.sgnC[R];
+  int pc = F.S<uint16_t>(F.L->s_pcol)[R];
+  int nd = 0;
+  for (int t = 0; t < deg; ++t) {
+    int c = chk_nb(C, R, t);
+    if (c == pc) continue;
+    uint16_t rr = poc[c];
+    if (rr != NONE16) deps[nd++] = (int)rr | (int)(((unsigned)(s >> t) & 1u) << 31);
+  }
+  return nd;
+}
+__device__ __forceinline__ int fwd_deps(const Frame& F, int R, int* deps) {
+  const DCode& C = *F.C;
+  int c = F.S<uint16_t>(F.L->s_pcol)[R];
+  int nd = 0;
+  if (c < C.n) {
+    uint8_t s = F.sgnV[c];
+    int dv = C.var_deg[c];
+    for (int k = 0; k < dv; ++k) {
+      if (!((s >> k) & 1)) continue;
+      int j = var_ck(C, c, k);
+      if (j == R) continue;
+      deps[nd++] = j | (int)(((unsigned)(s >> (4 + k)) & 1u) << 31);
+    }
+  }
+  return nd;
+}
+// sign of the diagonal entry A[R, C_k]
+__device__ __forceinline__ int diag_neg(const Frame& F, int R) {
+  const DCode& C = *F.C;
+  int c = F.S<uint16_t>(F.L->s_pcol)[R];
+  if (c >= C.n) return 0;
+  uint8_t s = F.sgnV[c];
+  int dv = C.var_deg[c];
+  for (int k = 0; k < dv; ++k)
+    if (var_ck(C, c, k) == R) return (s >> (4 + k)) & 1;
+  return 0;
+}
+
+// Dependency level of every pivot for one sweep (level = 1 + max level of its deps).
+// Pivots are processed in chunks of 32 in dependency order (fwd: ascending k, back:
+// descending k); dependencies inside the chunk are resolved by shuffle fixed-point rounds.
+// lv is indexed by pivot k.  Returns the number of levels.
+template <bool FWD>
+__device__ int compute_levels(const Frame& F, int p, uint16_t* lv) {
+  const uint16_t* prow = F.S<uint16_t>(F.L->s_prow);
+  const uint16_t* pos = F.S<uint16_t>(F.L->s_pos);
+  int maxlv = 0;
+  for (int c0 = 0; c0 < p; c0 += 32) {
+    int k = FWD ? (c0 + F.lane) : (p - 1 - c0 - F.lane);
+    bool valid = FWD ? (k < p) : (k >= 0);
+    int deps[DCMAX];
+    int nd = 0;
+    if (valid) {
+      int R = prow[k];
+      nd = FWD ? fwd_deps(F, R, deps) : back_deps(F, R, deps);
+    }
+    int ext = 0, nin = 0;
+    int inl[DCMAX];
+    for (int d = 0; d < nd; ++d) {
+      int kd = pos[deps[d] & 0x7fffffff];
+      int off = FWD ? (kd - c0) : (p - 1 - c0 - kd);
+      if (off >= 0 && off < 32) inl[nin++] = off;
+      else ext = max(ext, (int)lv[kd] + 1);
+    }
+    int ninmax = wmaxi(nin);
+    int cur = ext;
+    for (int it = 0; it <= 32; ++it) {
+      int nw = ext;
+      for (int d = 0; d < ninmax; ++d) {
+        int src = (d < nin) ? inl[d] : F.lane;
+        int vv = __shfl_sync(FULL, cur, src);
+        if (d < nin) nw = max(nw, vv + 1);
+      }
+      bool ch = (nw != cur);
+      cur = nw;
+      if (!__any_sync(FULL, ch)) break;
+    }
+    if (valid) {
+      lv[k] = (uint16_t)cur;
+      maxlv = max(maxlv, cur);
+    }
+    __syncwarp();
+  }
+  return wmaxi(maxlv) + 1;
+}
+
+// Deterministic counting sort of pivots by level: lv[k] (level) is replaced by the slot of
+// pivot k in level order; off[0..nL] (global) receives the level boundaries.
+__device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* off) {
+  int* hist = F.S<int>(F.L->s_hist);
+  int* cur = F.S<int>(F.L->s_cur);
+  for (int l = F.lane; l <= nL; l += 32) hist[l] = 0;
+  __syncwarp();
+  for (int k = F.lane; k < p; k += 32) atomicAdd(&hist[lv[k]], 1);
+  __syncwarp();
+  int carry = 0;
+  for (int b0 = 0; b0 < nL; b0 += 32) {  // exclusive prefix sum
+    int l = b0 + F.lane;
+    int hv = (l < nL) ? hist[l] : 0;
+    int incl = hv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(FULL, incl, o);
+      if (F.lane >= o) incl += t;
+    }
+    if (l < nL) {
+      off[l] = carry + incl - hv;
+      cur[l] = carry + incl - hv;
+    }
+    carry += __shfl_sync(FULL, incl, 31);
+  }
+  if (F.lane == 0) off[nL] = carry;
+  __syncwarp();
+  const unsigned lt = (1u << F.lane) - 1u;
+  for (int b0 = 0; b0 < p; b0 += 32) {
+    int k = b0 + F.lane;
+    bool valid = k < p;
+    int lvl = valid ? (int)lv[k] : -1 - F.lane;
+    unsigned peers = __match_any_sync(FULL, lvl);
+    int slot = 0;
+    if (valid) slot = cur[lvl] + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == F.lane) cur[lvl] += __popc(peers);
+    if (valid) lv[k] = (uint16_t)slot;
+    __syncwarp();
+  }
+}
+
+// Builds both sweep programs.  Record layout (ints):
+//  back  recB[slot*RB]: head = R | nd << 24 | diag_neg << 31, then nd deps (row | neg << 31)
+//  fwd   recF[slot*RF]: same head/deps; dinvF[slot] = 1 / d^2 of the pivot column
+__device__ void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  sort_columns(F);
+  peel_columnwise(F, p);
+  uint16_t* poc = F.S<uint16_t>(L.s_poc);
+  const uint16_t* prow = F.S<uint16_t>(L.s_prow);
+  const uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
+  for (int c = F.lane; c < C.Q; c += 32) poc[c] = NONE16;
+  __syncwarp();
+  for (int k = F.lane; k < p; k += 32) {
+    int R = prow[k];
+    poc[pcol[R]] = (uint16_t)R;
+  }
+  __syncwarp();
+  uint16_t* lvB = F.S<uint16_t>(L.s_lvB);
+  uint16_t* lvF = F.S<uint16_t>(L.s_lvF);
+  nLb = compute_levels<false>(F, p, lvB);
+  nLf = compute_levels<true>(F, p, lvF);
+  level_slots(F, p, nLb, lvB, F.offB);
+  level_slots(F, p, nLf, lvF, F.offF);
+  for (int k = F.lane; k < p; k += 32) {
+    int R = prow[k];
+    int deps[DCMAX];
+    int dn = diag_neg(F, R);
+    int nd = back_deps(F, R, deps);
+    int* rb = F.recB + (size_t)lvB[k] * C.RB;
+    rb[0] = R | (nd << 24) | (int)((unsigned)dn << 31);
+    for (int d = 0; d < nd; ++d) rb[1 + d] = deps[d];
+    nd = fwd_deps(F, R, deps);
+    int sf = lvF[k];
+    int* rf = F.recF + (size_t)sf * RF;
+    rf[0] = R | (nd << 24) | (int)((unsigned)dn << 31);
+    for (int d = 0; d < nd; ++d) rf[1 + d] = deps[d];
+    F.dinvF[sf] = 1.0 / F.d2[pcol[R]];
+  }
+  __syncwarp();
+}
+
+// Pivot sequence output (ipm_step_pcg debug/parity): rows[k], cols[k], -1 past p.
+__device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
+  const DCode& C = *F.C;
+  const uint16_t* prow = F.S<uint16_t>(F.L->s_prow);
+  const uint16_t* pcol = F.S<uint16_t>(F.L->s_pcol);
+  for (int k = F.lane; k < C.m; k += 32) {
+    int R = (k < p) ? (int)prow[k] : -1;
+    if (rows) rows[k] = R;
+    if (cols) cols[k] = (k < p) ? (int)pcol[R] : -1;
+  }
+}
+
+// =====================================================================================
+// PCG (Alg. 4) on (A D^2 A^T) dy = w with x^0 = 0 (C-9), matrix-free:
+//   l = A (D^2 (A^T h)):  t_i = sum_j A_ji h_j (per variable), l_j = sum_i A_ji d2_i t_i
+//                         + d2_{n+j} h_j (per check)                   [eq.`Delta y` LHS]
+//   M^-1 r: back sweep A_M f = r, scale by D_M^-2, forward sweep A_M^T z = f
+// Stops after line 9 once ||r||_2 <= tol ||w||_2 (G15).  h^T l <= 0 -> breakdown.
+// w is read from F.w; the solution accumulates in F.dy.
+// =====================================================================================
+__device__ __forceinline__ void precond_apply(const Frame& F, bool use_mtm, int nLb, int nLf,
+                                              double& rz) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  double* rS = F.S<double>(L.s_r);
+  double* fS = F.S<double>(L.s_f);
+  double* zS = F.S<double>(L.s_z);
+  double acc_rz = 0.0;
+  if (!use_mtm) {
+    for (int j = F.lane; j < C.m; j += 32) {
+      double r = rS[j];
+      zS[j] = r;
+      acc_rz += r * r;
+    }
+    __syncwarp();
+    rz = wsum(acc_rz);
+    return;
+  }
+  const int RB = C.RB;
+  for (int lvl = 0; lvl < nLb; ++lvl) {
+    int s0 = F.offB[lvl], s1 = F.offB[lvl + 1];
+    for (int s = s0 + F.lane; s < s1; s += 32) {
+      const int* rec = F.recB + (size_t)s * RB;
+      int head = rec[0];
+      int R = head & 0xffffff, nd = (head >> 24) & 0xf;
+      double acc = rS[R];
+      for (int d = 0; d < nd; ++d) {
+        int dep = rec[1 + d];
+        double fv = fS[dep & 0x7fffffff];
+        acc = (dep < 0) ? acc + fv : acc - fv;
+      }
+      fS[R] = (head < 0) ? -acc : acc;
+    }
+    __syncwarp();
+  }
+  for (int lvl = 0; lvl < nLf; ++lvl) {
+    int s0 = F.offF[lvl], s1 = F.offF[lvl + 1];
+    for (int s = s0 + F.lane; s < s1; s += 32) {
+      const int* rec = F.recF + (size_t)s * RF;
+      int head = rec[0];
+      int R = head & 0xffffff, nd = (head >> 24) & 0xf;
+      double acc = fS[R] * F.dinvF[s];
+      for (int d = 0; d < nd; ++d) {
+        int dep = rec[1 + d];
+        double zv = zS[dep & 0x7fffffff];
+        acc = (dep < 0) ? acc + zv : acc - zv;
+      }
+      double zz = (head < 0) ? -acc : acc;
+      zS[R] = zz;
+      acc_rz += zz * rS[R];
+    }
+    __syncwarp();
+  }
+  rz = wsum(acc_rz);
+}
+
+struct PcgResult {
+  int iters, status;
+  double relres;
+};
+
+__device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, int nLb, int nLf) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  double* hS = F.S<double>(L.s_h);
+  double* rS = F.S<double>(L.s_r);
+  double* zS = F.S<double>(L.s_z);
+  double* tS = F.S<double>(L.s_t);
+  double* fS = F.S<double>(L.s_f);
+  // line 1-2: x^0 = 0, r^0 = w
+  double ww = 0.0;
+  for (int j = F.lane; j < C.m; j += 32) {
+    bool pr = (F.sgnC[j] & PRESENT) != 0;
+    double wj = pr ? F.w[j] : 0.0;
+    rS[j] = wj;
+    zS[j] = 0.0;
+    fS[j] = 0.0;
+    F.dy[j] = 0.0;
+    ww += wj * wj;
+  }
+  __syncwarp();
+  double wn = sqrt(wsum(ww));
+  PcgResult res{0, 0, 0.0};
+  if (wn == 0.0) {
+    for (int j = F.lane; j < C.m; j += 32) hS[j] = 0.0;
+    __syncwarp();
+    return res;
+  }
+  // line 3-4: z^0 = M^-1 r^0, h^0 = z^0
+  double rz;
+  precond_apply(F, use_mtm, nLb, nLf, rz);
+  for (int j = F.lane; j < C.m; j += 32) hS[j] = zS[j];
+  __syncwarp();
+  const double tol = P.pcg_rel_tol * wn;
+  res.status = ST_PCG_MAXITER;
+  res.relres = 1.0;
+  for (int it = 0; it < P.pcg_max_iter; ++it) {
+    // line 6: l = Q h (matrix-free)
+    for (int i = F.lane; i < C.n; i += 32) {
+      uint8_t s = F.sgnV[i];
+      if (!(s & 0xf)) continue;
+      int dv = C.var_deg[i];
+      double acc = 0.0;
+      for (int k = 0; k < dv; ++k) {
+        double hv = hS[var_ck(C, i, k)];  // absent rows hold h = 0
+        acc = ((s >> (4 + k)) & 1) ? acc - hv : acc + hv;
+      }
+      tS[i] = F.d2[i] * acc;
+    }
+    __syncwarp();
+    double hl = 0.0;
+    for (int j = F.lane; j < C.m; j += 32) {
+      uint16_t s = F.sgnC[j];
+      if (!(s & PRESENT)) continue;
+      int deg = C.chk_deg[j];
+      double hj = hS[j];
+      double acc = F.d2[C.n + j] * hj;
+      for (int t = 0; t < deg; ++t) {
+        double tv = tS[chk_nb(C, j, t)];
+        acc = ((s >> t) & 1) ? acc - tv : acc + tv;
+      }
+      F.l[j] = acc;
+      hl += hj * acc;
+    }
+    hl = wsum(hl);
+    if (!(hl > 0.0) || !isfinite(hl)) {
+      res.status = ST_PCG_BREAKDOWN;
+      break;
+    }
+    // lines 7-9
+    double alpha = rz / hl;
+    double rr = 0.0;
+    for (int j = F.lane; j < C.m; j += 32) {
+      if (!(F.sgnC[j] & PRESENT)) continue;
+      F.dy[j] += alpha * hS[j];
+      double r = rS[j] - alpha * F.l[j];
+      rS[j] = r;
+      rr += r * r;
+    }
+    __syncwarp();
+    rr = wsum(rr);
+    res.iters = it + 1;
+    res.relres = sqrt(rr) / wn;
+    if (sqrt(rr) <= tol) {
+      res.status = 0;
+      break;
+    }
+    // lines 10-12
+    double rz_new;
+    precond_apply(F, use_mtm, nLb, nLf, rz_new);
+    double nu = rz_new / rz;
+    rz = rz_new;
+    for (int j = F.lane; j < C.m; j += 32) {
+      if (!(F.sgnC[j] & PRESENT)) continue;
+      hS[j] = zS[j] + nu * hS[j];
+    }
+    __syncwarp();
+  }
+  return res;
+}
+
+}  // namespace alp

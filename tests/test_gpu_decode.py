@@ -1,0 +1,155 @@
+"""GPU parity of alp_decode (Alg. 3 + §IV-B IPM + Alg. 4/7) against the oracle.
+
+Gates:
+  P1 hard decisions bit-exact where the oracle's |u_i - 1/2| > 1e-3
+  P2 certificate bit-exact where |g_max - tau_cert| > 1e-3
+  P3 |obj_gpu - obj_oracle| <= 1e-6 max(1, |obj_oracle|)
+  P4 no PCG_MAXITER / breakdown / numeric status
+  P6 the O(E) LP-duality certificate holds on every GPU frame
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.lp import malp_decode
+from oracle.certify import dual_certificate_batch
+from synth import config_code, config_frames
+from synth.codes import code_from_dense, code_from_rows
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _alp():
+    import paper_0902_0657_b200 as alp
+    return alp
+
+
+def gpu_decode(code, llr, **pkw):
+    alp = _alp()
+    c = alp.Code.from_synth(code)
+    params = alp.default_params(**pkw)
+    res = alp.decode(c, torch.from_numpy(np.ascontiguousarray(llr)).cuda(), params, want_u=True,
+                     want_y=True, want_masks=True)
+    torch.cuda.synchronize()
+    assert alp.last_launch_count() == 1
+    return dict(hard=res.hard.cpu().numpy(), obj=res.objective.cpu().numpy(),
+                cert=res.certificate.cpu().numpy(), status=res.status.cpu().numpy(),
+                stats=res.stats_numpy(), u=res.u.cpu().numpy(), y=res.y.cpu().numpy(),
+                masks=res.masks.cpu().numpy().view(np.uint16))
+
+
+def compare(code, llr, g, frames, variant="A"):
+    """P1-P3 against the oracle on `frames`; returns diagnostics."""
+    lp_match = 0
+    for f in frames:
+        o = malp_decode(code, llr[f], variant)
+        u = o["u"]
+        sure = np.abs(u - 0.5) > 1e-3
+        assert np.array_equal(g["hard"][f][sure], o["hard"][sure]), f"frame {f}: hard decisions differ"
+        if abs(o["g_max"] - 1e-2) > 1e-3:
+            assert g["cert"][f] == o["cert"], f"frame {f}: certificate differs"
+        assert abs(g["obj"][f] - o["obj"]) <= 1e-6 * max(1.0, abs(o["obj"])), \
+            f"frame {f}: objective {g['obj'][f]} vs {o['obj']}"
+        lp_match += int(g["stats"]["lp_solves"][f] == o["lp_solves"])
+    return dict(lp_match=lp_match / max(1, len(frames)))
+
+
+def assert_certified(code, llr, g):
+    cert = dual_certificate_batch(code, llr, g["u"], g["y"], g["masks"])
+    bad = np.nonzero(~cert["ok"])[0]
+    assert bad.size == 0, f"P6 certificate fails on frames {bad[:10]} (gap {cert['gap'][bad[:5]]})"
+    assert np.all(g["status"] == 0), np.unique(g["status"], return_counts=True)
+
+
+def test_h7_golden_fractional_output():
+    g = json.load(open(os.path.join(GOLD, "h7_trace.json")))
+    code = code_from_dense(np.array([[int(c) for c in r] for r in g["H"]]))
+    llr = np.array([g["gamma"]])
+    for variant in (0, 1):
+        out = gpu_decode(code, llr, variant=variant)
+        np.testing.assert_allclose(out["u"][0], g["trace"][-1]["u"], atol=1e-7)
+        assert out["cert"][0] == 0
+        assert out["obj"][0] == pytest.approx(g["trace"][-1]["obj"], abs=1e-7)
+        assert out["stats"]["lp_solves"][0] == len(g["trace"])
+        assert out["stats"]["max_p"][0] == 3
+
+
+def test_h1_examples_and_zero_lp_frames():
+    code = code_from_rows([[0, 1, 2], [1, 2, 3]], 4, "H1")
+    llr = np.array([[-3.0, 1.0, 2.0, -1.0], [1.0, 1.0, 1.0, 1.0], [-1.0, -2.0, 3.0, 4.0]])
+    out = gpu_decode(code, llr)
+    np.testing.assert_allclose(out["u"][0], [1, 1, 0, 1], atol=1e-7)
+    assert list(out["cert"]) == [1, 1, 1]
+    assert out["stats"]["lp_solves"][1] == 0 and out["obj"][1] == 0.0     # C-15
+    assert out["stats"]["lp_solves"][2] == 0 and out["obj"][2] == -3.0
+
+
+@pytest.mark.parametrize("variant", ["A", "B"])
+def test_config1_all_frames(variant):
+    code = config_code(1)
+    fb = config_frames(1)
+    g = gpu_decode(code, fb.llr, variant=0 if variant == "A" else 1)
+    diag = compare(code, fb.llr, g, range(fb.F), variant)
+    assert_certified(code, fb.llr, g)
+    print(f"C1 MALP-{variant}: LP-count match {diag['lp_match']:.2f}; "
+          f"mean PCG iters/frame {g['stats']['pcg_iters'].mean():.1f}")
+
+
+@pytest.mark.parametrize("snr_idx", [0, 2])
+def test_config2_sample(snr_idx):
+    code = config_code(2)
+    fb = config_frames(2, snr_idx, frames=range(256))
+    g = gpu_decode(code, fb.llr)
+    assert_certified(code, fb.llr, g)
+    compare(code, fb.llr, g, range(12))
+    # sanity: certified frames decode to a codeword no worse than the transmitted one
+    tx_cost = (fb.codewords * fb.llr).sum(axis=1)
+    cf = g["cert"] == 1
+    assert np.all(g["obj"][cf] <= tx_cost[cf] + 1e-6)
+
+
+def test_config3_sample():
+    code = config_code(3)
+    fb = config_frames(3, frames=range(64))
+    g = gpu_decode(code, fb.llr)
+    assert_certified(code, fb.llr, g)
+    compare(code, fb.llr, g, range(4))
+
+
+@pytest.mark.parametrize("F", [1, 37])
+def test_ragged_batches_and_determinism(F):
+    code = config_code(1)
+    fb = config_frames(1, frames=range(F))
+    a = gpu_decode(code, fb.llr)
+    b = gpu_decode(code, fb.llr)
+    for k in ("hard", "obj", "cert", "u", "y", "masks"):
+        assert np.array_equal(a[k], b[k]), k
+    compare(code, fb.llr, a, range(min(F, 5)))
+
+
+def test_empty_batch_and_extreme_llrs():
+    alp = _alp()
+    code = config_code(1)
+    c = alp.Code.from_synth(code)
+    r = alp.decode(c, torch.zeros((0, code.n), dtype=torch.float64, device="cuda"))
+    assert r.hard.shape == (0, code.n)
+    fb = config_frames(1, frames=range(8))
+    llr = fb.llr * 100.0
+    g = gpu_decode(code, llr)
+    assert_certified(code, llr, g)
+    compare(code, llr, g, range(4))
+
+
+@pytest.mark.slow
+def test_config2_full_batch_certified():
+    """16,384 frames at 2.0 dB (the bench workload): every frame certified (P6), every PCG
+    solve converged (P4), sampled oracle parity."""
+    code = config_code(2)
+    fb = config_frames(2, 0)
+    g = gpu_decode(code, fb.llr)
+    assert_certified(code, fb.llr, g)
+    compare(code, fb.llr, g, np.random.default_rng(1).choice(fb.F, 6, replace=False))

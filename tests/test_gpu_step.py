@@ -1,0 +1,137 @@
+"""GPU parity of ipm_step_pcg (eq.`Delta y` P:479 by Alg. 4 + Alg. 7) against the oracle.
+
+Gates (SURVEY C-27): pivot sequence bit-exact vs the oracle's heap Alg. 7
+on identical weights; recursive ||r||/||w|| <= 1e-8; ||dy - dy_chol|| / ||dy_chol|| <= 1e-8
+against the oracle's fp64 Cholesky (well-conditioned cases are gated tighter).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.lp import cholesky_solve, normal_matrix
+from oracle.precond import mts_columnwise
+from synth import config_code, c5_systems
+from synth.codes import code_from_rows
+from tests.helpers import dense_step_matrix, step_weights, oracle_col_to_gpu
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _alp():
+    import paper_0902_0657_b200 as alp
+    return alp
+
+
+def _t(x, dtype=None):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+
+
+def _run(code, masks, d, r, flip=None, **pkw):
+    alp = _alp()
+    c = alp.Code.from_synth(code)
+    params = alp.default_params(**pkw)
+    res = alp.ipm_step_pcg(c, _t(masks.view(np.int16)), _t(d), _t(r),
+                           None if flip is None else _t(flip.astype(np.uint8)), params=params,
+                           want_pivots=True)
+    torch.cuda.synchronize()
+    assert alp.last_launch_count() == 1
+    return dict(dy=res.dy.cpu().numpy(), iters=res.iters.cpu().numpy(), relres=res.relres.cpu().numpy(),
+                status=res.status.cpu().numpy(), prow=res.pivot_rows.cpu().numpy(),
+                pcol=res.pivot_cols.cpu().numpy())
+
+
+def _check_system(code, mk, dd, rr, fl, out, s, tol_dy=1e-8, check_pivots=True):
+    A, rows = dense_step_matrix(code, mk, fl)
+    w2 = step_weights(code, dd, rows)
+    if check_pivots:
+        col, row = mts_columnwise(A, w2)
+        exp_rows = [rows[rw] for rw in row]
+        exp_cols = [oracle_col_to_gpu(code, rows, c) for c in col]
+        p = len(rows)
+        assert list(out["prow"][s][:p]) == exp_rows, f"system {s}: pivot rows differ"
+        assert list(out["pcol"][s][:p]) == exp_cols, f"system {s}: pivot cols differ"
+        assert np.all(out["prow"][s][p:] == -1)
+    Q = normal_matrix(A, w2)
+    ref = cholesky_solve(Q, rr[rows])
+    got = out["dy"][s][rows]
+    assert out["status"][s] == 0, f"system {s} status {out['status'][s]}"
+    assert out["relres"][s] <= 1e-8
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= tol_dy, f"system {s}: rel err {err:.3e}"
+    absent = [j for j in range(code.m) if j not in set(rows)]
+    assert np.all(out["dy"][s][absent] == 0.0)
+    return err
+
+
+def test_golden_step_system():
+    g = json.load(open(os.path.join(GOLD, "precond_examples.json")))["step_system"]
+    code = code_from_rows([[0, 1], [1, 2]], 3)
+    masks = np.array([[0x8003, 0x8003]], dtype=np.uint16)       # all coefficients +1
+    d = np.ones((1, 5))
+    r = np.array([g["r"]], dtype=np.float64)
+    out = _run(code, masks, d, r)
+    np.testing.assert_allclose(out["dy"][0], g["dy"], rtol=1e-14)
+    assert list(out["prow"][0]) == g["pivots_row"]
+    assert list(out["pcol"][0]) == g["pivots_col"]
+
+
+def test_c5_shaped_systems_vs_oracle():
+    code = config_code(5)
+    sy = c5_systems(range(24), code)
+    out = _run(code, sy.masks, sy.d, sy.r)
+    errs = [_check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, s) for s in range(sy.S)]
+    print("C5 rel err max %.2e, iters %s" % (max(errs), out["iters"].tolist()))
+
+
+@pytest.mark.parametrize("S", [1, 33, 130])
+def test_partial_rows_flips_and_ragged_batches(S):
+    code = config_code(1)
+    rng = np.random.default_rng(S)
+    sy = c5_systems(range(S), code, lo=-3, hi=3, present_frac=0.6)
+    flip = rng.integers(0, 2, size=(S, code.n)).astype(np.uint8)
+    out = _run(code, sy.masks, sy.d, sy.r, flip)
+    for s in range(S):
+        if (sy.masks[s] >> 15).sum() == 0:
+            continue
+        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], flip[s], out, s, tol_dy=1e-9)
+
+
+def test_plain_cg_option():
+    code = config_code(1)
+    sy = c5_systems(range(8), code, lo=-0.2, hi=0.2)
+    out = _run(code, sy.masks, sy.d, sy.r, precond=1)
+    assert np.all(out["prow"] == -1)
+    for s in range(8):
+        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, s, tol_dy=1e-8, check_pivots=False)
+
+
+def test_empty_batch_and_all_absent_rows():
+    alp = _alp()
+    code = config_code(1)
+    c = alp.Code.from_synth(code)
+    z = torch.zeros((0, code.m), dtype=torch.int16, device="cuda")
+    res = alp.ipm_step_pcg(c, z, torch.zeros((0, code.n + code.m), dtype=torch.float64, device="cuda"),
+                           torch.zeros((0, code.m), dtype=torch.float64, device="cuda"))
+    assert res.dy.shape == (0, code.m)
+    masks = np.zeros((2, code.m), dtype=np.uint16)
+    out = _run(code, masks, np.ones((2, code.n + code.m)), np.ones((2, code.m)))
+    assert np.all(out["dy"] == 0) and np.all(out["iters"] == 0) and np.all(out["status"] == 0)
+
+
+@pytest.mark.slow
+def test_c5_full_size_properties_and_sampled_parity():
+    """All 65,536 config-5 systems in the bench launch configuration: every system converges
+    to 1e-8 (property at any size); 16 sampled systems match the oracle (pivots + Cholesky)."""
+    code = config_code(5)
+    S = 65536
+    sy = c5_systems(range(S), code)
+    out = _run(code, sy.masks, sy.d, sy.r)
+    assert np.all(out["status"] == 0), np.unique(out["status"], return_counts=True)
+    assert np.all(out["relres"] <= 1e-8)
+    for s in np.random.default_rng(0).choice(S, 16, replace=False):
+        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, int(s))
