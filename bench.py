@@ -1,0 +1,361 @@
+"""Benchmark of the batched ALP decoder (libalp.so) — the driver's bench contract.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  (N > 1: launched by torch.distributed.run, one rank per GPU)
+
+Workload = BASELINE.json configs[1] ("C2"): random (3,6)-regular LDPC code n=1000, m=500,
+16,384 frames per rank of random codewords, BPSK/AWGN at Eb/N0 = 2.0 dB (the hardest of the
+config's three SNRs; --snr-idx picks another), fp64 LLR costs.  One STEP = one alp_decode
+call over the whole batch: MALP-A cut search, every LP solved by the primal-dual IPM, every
+Newton step by PCG with the column-wise triangular preconditioner.
+
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+launching stream; between timed steps a 256 MiB buffer is written to flush L2 (outside the
+events).  Inputs (131 MB of LLRs) are device-resident for `value`; `e2e` repeats the step
+through alp_decode_host from pinned host memory (H2D + D2H inside the timed region).
+Frames shard across ranks (frame f -> rank f mod N, no data-path collective; counters are
+all-reduced once at the end), so `scaling` is "weak" (16,384 frames per GPU).
+
+The oracle (oracle/, fp64 numpy, dense Cholesky step solve) is timed on the host cores on
+a bounded sample (cpu_baseline; and `--impl reference`).  It is never on the product path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np
+
+METRIC = "LP-decoded frames/sec, (3,6) LDPC n=1000; PCG HBM GB/s vs ~8 TB/s peak"
+UNIT = "frames/s"
+FRAMES_PER_RANK = 16384
+SNRS = [2.0, 2.5, 3.0]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--snr-idx", type=int, default=0)
+    ap.add_argument("--frames", type=int, default=FRAMES_PER_RANK, help="frames per rank")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_config(args, ws):
+    return {
+        "workload": f"C2: random (3,6)-regular LDPC n=1000 m=500, {args.frames} random-codeword "
+                    f"frames per GPU, BPSK/AWGN Eb/N0={SNRS[args.snr_idx]} dB, fp64 LLR, MALP-A + "
+                    "primal-dual IPM + PCG (column-wise MTS preconditioner) to rel. residual 1e-8",
+        "code": "rnd(3,6) n=1000 m=500 seed 1002",
+        "frames_per_gpu": args.frames,
+        "global_frames": args.frames * ws,
+        "ebn0_db": SNRS[args.snr_idx],
+        "parallelism": f"frame-sharded dp{ws}",
+        "l2": "256 MiB L2 flush between timed steps (LLR input 131 MB also exceeds L2)",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def _oracle_worker(args_tuple):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)   # one BLAS thread per worker process
+    snr_idx, frames = args_tuple
+    from synth import config_code, config_frames
+    from oracle.lp import malp_decode
+    code = config_code(2)
+    fb = config_frames(2, snr_idx, frames=frames, code=code)
+    t0 = time.perf_counter()
+    for f in range(fb.F):
+        malp_decode(code, fb.llr[f])
+    return fb.F, time.perf_counter() - t0
+
+
+def time_oracle(snr_idx: int, budget_s: float, frame_offset: int = 0):
+    """Oracle MALP-A decode (fp64, dense Cholesky) on the host cores: one frame per worker
+    process, frames taken in order from frame_offset, workers run until budget_s elapses.
+    Returns (frames/s, cores, frames decoded)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    per = 2
+    t0 = time.perf_counter()
+    done, nxt = 0, frame_offset
+    ctx = mp.get_context("fork")
+    env_threads = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_threads:
+        os.environ[k] = "1"
+    try:
+        with ctx.Pool(cores) as pool:
+            while True:
+                jobs = [(snr_idx, list(range(nxt + w * per, nxt + (w + 1) * per))) for w in range(cores)]
+                nxt += cores * per
+                for F, _ in pool.map(_oracle_worker, jobs):
+                    done += F
+                if time.perf_counter() - t0 >= budget_s:
+                    break
+    finally:
+        for k, v in env_threads.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    wall = time.perf_counter() - t0
+    return done / wall, cores, done, wall
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    times, frames = [], 0
+    budget = max(2.0, min(args.cpu_seconds, 60.0))
+    for s in range(args.warmup + args.steps):
+        fps, cores, nf, wall = time_oracle(args.snr_idx, budget / 2, frame_offset=0)
+        if s >= args.warmup:
+            times.append(wall)
+            frames += nf
+    v = frames / sum(times)
+    sample = (f"MALP-A oracle (fp64 numpy, dense Cholesky step solve) on the first frames of the "
+              f"config, {cores} worker processes x 1 BLAS thread, ~{budget / 2:.0f} s per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args, ws),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device (no CPU fallback)"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_0902_0657_b200 as alp
+    from paper_0902_0657_b200.dist import shard_frame_ids, frame_counters, reduce_run
+    from synth import config_code, config_frames
+
+    code = config_code(2)
+    # this rank's frames: global frame g = rank + ws * t (interleaved sharding)
+    frame_ids = shard_frame_ids(args.frames, rank, ws)
+    fb = config_frames(2, args.snr_idx, frames=frame_ids, code=code)
+    llr_host = torch.from_numpy(fb.llr).pin_memory()
+    llr = llr_host.to(dev)
+    c = alp.Code.from_synth(code)
+    stream = torch.cuda.current_stream(dev)
+    F = args.frames
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = alp.decode(c, llr, stream=stream)      # allocates outputs + workspace once
+    torch.cuda.synchronize(dev)
+
+    def step():
+        alp.decode(c, llr, stream=stream, out=out)
+        return alp.last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.3)
+    launches = 0
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)
+        ev[k][0].record(stream)
+        launches += step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    if ws > 1:
+        dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t_rank = sum(ms) / 1e3
+
+    # per-frame counters of the last step (identical every step: deterministic decode)
+    st = out.stats_numpy()
+    counters = frame_counters(out.hard.cpu().numpy(), fb.codewords, out.certificate.cpu().numpy(),
+                              out.status.cpu().numpy(), st)
+    pcg_bytes = float(counters[7])
+
+    # e2e through the host API (pinned host LLRs in, host outputs back, inside the timing)
+    e2e_t = 0.0
+    if not args.no_e2e:
+        hout = dict(hard=torch.empty((F, code.n), dtype=torch.uint8, pin_memory=True),
+                    objective=torch.empty(F, dtype=torch.float64, pin_memory=True),
+                    certificate=torch.empty(F, dtype=torch.uint8, pin_memory=True),
+                    status=torch.empty(F, dtype=torch.int32, pin_memory=True))
+        alp.decode_host(c, llr_host, stream=stream, out=hout)
+        torch.cuda.synchronize(dev)
+        e2e_ms = []
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            alp.decode_host(c, llr_host, stream=stream, out=hout)   # synchronises internally
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            e2e_ms.append(a.elapsed_time(b))
+        e2e_t = sum(e2e_ms) / 1e3
+        h2d = F * code.n * 8
+        d2h = F * code.n + F * 8 + F + F * 4
+    allc, t_max = reduce_run(counters, t_rank, device=dev)
+    _, e2e_max = reduce_run(counters[:1], e2e_t, device=dev)
+    counters, pcg_bytes_all = allc, float(allc[7])
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    total_frames = F * ws * args.steps
+    value = total_frames / t_max
+    peak, peak_kind = measured_peak_hbm()
+    # dominant (only) kernel: alp_decode_kernel, one launch per step on `stream`
+    achieved = pcg_bytes / (t_rank / args.steps) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, ws),
+        "gpu_launches": launches,
+        "clocks": clk,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "alp_decode_kernel",
+                     "bytes": "sum over executed PCG iterations of B_min(p,n_act,m) (DESIGN.md §6)",
+                     "peak_kind": peak_kind},
+        "pcg": {"iters_per_s": counters[5] / (t_max / args.steps),
+                "iters_total_per_step": int(counters[5]),
+                "gbs_all_ranks": pcg_bytes_all / (t_max / args.steps) / 1e9},
+        "decode": {"frames": int(counters[0]), "frame_errors": int(counters[1]),
+                   "not_certified": int(counters[2]), "lp_solves": int(counters[3]),
+                   "ipm_iters": int(counters[4]), "status_nonzero": int(counters[6])},
+        "step_ms": ms,
+    }
+    if not args.no_e2e:
+        line["e2e"] = {"value": total_frames / e2e_max, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if ws == 1 and not args.no_cpu_baseline:
+        fps, cores, nf, wall = time_oracle(args.snr_idx, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": fps, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {nf} frames of the same workload, MALP-A oracle (fp64 numpy, dense "
+                      f"Cholesky), {cores} worker processes x 1 BLAS thread, {wall:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -71,7 +71,13 @@ typedef enum {
   ALP_FRAME_IPM_MAXITER = 2,     /* some LP hit ipm_max_iter Newton steps                   */
   ALP_FRAME_PCG_MAXITER = 4,     /* some PCG solve ended above pcg_rel_tol at pcg_max_iter  */
   ALP_FRAME_PCG_BREAKDOWN = 8,   /* some PCG solve met h^T Q h <= 0 (or non-finite)          */
-  ALP_FRAME_NUMERIC = 16         /* non-finite IPM iterate; decoding of the frame stopped   */
+  ALP_FRAME_NUMERIC = 16,        /* non-finite IPM iterate; decoding of the frame stopped   */
+  ALP_FRAME_PCG_FLOOR = 32,      /* informational: some PCG solve stopped with its TRUE
+                                    residual at the fp64 evaluation floor
+                                    16 eps || |A| D^2 |A|^T |dy| ||_2, above pcg_rel_tol ||w|| */
+  ALP_FRAME_PCG_FALLBACK = 64    /* informational: some MTS-preconditioned PCG run broke down
+                                    or failed the true-residual test, and the solve was redone
+                                    by plain CG; the better result was kept (R-2) */
 } alp_frame_status;
 
 typedef struct alp_code alp_code;   /* opaque, immutable after creation */
@@ -93,7 +99,9 @@ typedef struct {
   double eta;             /* step damping of the ratio test (C-6)                0.99   */
   double gap_tol;         /* stop: x^T z <= gap_tol * (1 + |c^T x|) (C-8)               1e-9   */
   double feas_tol;        /* stop: ||r_b||, ||r_c|| <= feas_tol * (1 + ||b||, ||c||)    1e-8   */
-  double pcg_rel_tol;     /* PCG stop: ||r||_2 <= pcg_rel_tol * ||w||_2 (C-9, G15)      1e-8   */
+  double pcg_rel_tol;     /* PCG stop: ||r||_2 <= pcg_rel_tol * ||w||_2 (C-9, G15) on the
+                             recursive residual, then verified on the TRUE residual
+                             w - Q dy (restart from it if needed; R-1)      1e-8   */
   double tau_viol;        /* cut violated iff lhs < 1 - tau_viol (C-3)                  1e-6   */
   double tau_act;         /* cut active iff slack <= tau_act (C-4)                      1e-6   */
   double tau_cert;        /* certificate needs g_max <= tau_cert (C-11)                 1e-2   */
@@ -159,7 +167,7 @@ size_t alp_pcg_workspace_bytes(const alp_code* code, int64_t n_sys, const alp_pa
  *   d [n_sys][n + m] fp64 > 0, the diagonal of D (entries of absent slack columns ignored);
  *   r [n_sys][m] fp64 right-hand side (absent rows ignored).
  * Outputs (DEVICE): dy [n_sys][m] (0 on absent rows); optional (NULL to skip):
- *   pcg_iters [n_sys] int32, rel_res [n_sys] fp64 (recursive ||r||/||w||),
+ *   pcg_iters [n_sys] int32, rel_res [n_sys] fp64 (TRUE ||w - Q dy|| / ||w|| at exit),
  *   sys_status [n_sys] int32 (ALP_FRAME_PCG_* bits),
  *   pivot_rows / pivot_cols [n_sys][m] int32: the preconditioner's pivot sequence
  *   (Alg. 7 pick k: row pivot_rows[s][k], column pivot_cols[s][k] in 0..n+m-1, slack of

@@ -13,6 +13,7 @@ Adaptive LP decoding written out step by step from PAPER.md:
                        P:496-500 with sigma (C-5), ratio test (C-6), start (C-7),
                        stopping rule (C-8).  The step solve is DIRECT (Cholesky of
                        the dense A D^2 A^T; safeguard C-29) — no PCG.
+  step_solve_exact     dy = (A D^2 A^T)^-1 w in extended precision (reference for PCG parity)
   malp_decode          Alg. 3 MALP-A P:220-240; MALP-B P:242; plain ALP Alg. 1
   decode_outputs       hard decision, objective gamma^T u, ML certificate (C-11, C-14)
 
@@ -157,6 +158,47 @@ def cholesky_solve(Q: np.ndarray, w: np.ndarray, info: dict | None = None) -> np
             info["chol_fixes"] = info.get("chol_fixes", 0) + nfix
     t = sla.solve_triangular(L, w, lower=True)
     return sla.solve_triangular(L.T, t, lower=False)
+
+
+def step_solve_exact(A, d2: np.ndarray, w: np.ndarray, refine: int = 4) -> np.ndarray:
+    """dy = Q^-1 w, Q = A D^2 A^T (eq.`Delta y`), to full fp64 accuracy even when
+    kappa(Q) ~ 1e18 (config 5, d^2 over 24 decades; SURVEY C-27).
+
+    The plain definition computed in extended precision: Q is formed in numpy longdouble
+    (x87 80-bit, eps 1.1e-19; A is +-1/0 and d2 fp64, so the products are exact), factored
+    by a textbook column Cholesky in longdouble, and the solution is iteratively refined
+    with longdouble residuals w - Q dy (converges while kappa * 1e-19 < 1).  Reference for
+    the GPU PCG parity of ipm_step_pcg; fp64 Cholesky (cholesky_solve) cannot serve there
+    because its own forward error reaches kappa * eps."""
+    A = np.asarray(A.todense()) if sp.issparse(A) else np.asarray(A)
+    ld = np.longdouble
+    Al = A.astype(ld)
+    Q = (Al * np.asarray(d2, dtype=np.float64).astype(ld)) @ Al.T
+    p = Q.shape[0]
+    if p == 0:
+        return np.zeros(0)
+    L = np.zeros_like(Q)
+    for k in range(p):
+        dkk = Q[k, k] - L[k, :k] @ L[k, :k]
+        if not dkk > 0:
+            raise np.linalg.LinAlgError("Q not numerically SPD in extended precision")
+        L[k, k] = np.sqrt(dkk)
+        L[k + 1:, k] = (Q[k + 1:, k] - L[k + 1:, :k] @ L[k, :k]) / L[k, k]
+
+    def solve(b):
+        t = np.zeros(p, dtype=ld)
+        for k in range(p):
+            t[k] = (b[k] - L[k, :k] @ t[:k]) / L[k, k]
+        y = np.zeros(p, dtype=ld)
+        for k in range(p - 1, -1, -1):
+            y[k] = (t[k] - L[k + 1:, k] @ y[k + 1:]) / L[k, k]
+        return y
+
+    wl = np.asarray(w, dtype=np.float64).astype(ld)
+    y = solve(wl)
+    for _ in range(refine):
+        y = y + solve(wl - Q @ y)
+    return y.astype(np.float64)
 
 
 def normal_matrix(A, d2: np.ndarray) -> np.ndarray:

@@ -18,6 +18,7 @@ from ._ffi import AlpParams, STATS_FIELDS
 STATUS_NAMES = {0: "ALP_OK", -1: "ALP_ERR_INVALID_ARG", -2: "ALP_ERR_BAD_CODE",
                 -3: "ALP_ERR_UNSUPPORTED", -4: "ALP_ERR_CUDA", -5: "ALP_ERR_WORKSPACE"}
 FRAME_ALP_MAXITER, FRAME_IPM_MAXITER, FRAME_PCG_MAXITER, FRAME_PCG_BREAKDOWN, FRAME_NUMERIC = 1, 2, 4, 8, 16
+FRAME_PCG_FLOOR, FRAME_PCG_FALLBACK = 32, 64   # informational (include/alp.h)
 STATS_DTYPE = np.dtype(STATS_FIELDS)
 
 

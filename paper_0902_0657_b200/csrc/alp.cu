@@ -427,6 +427,7 @@ Layout make_layout(const DCode& C) {
   L.g_v = g(8 * Q);
   L.g_y = g(8 * m);
   L.g_dy = g(8 * m);
+  L.g_dyb = g(8 * m);
   L.g_l = g(8 * m);
   L.g_w = g(8 * m);
   L.g_u = g(8 * n);

@@ -22,7 +22,7 @@ constexpr int RF = 4;      // forward-record ints: head + up to d_v - 1 deps
 
 // frame status bits (include/alp.h alp_frame_status)
 constexpr int ST_ALP_MAXITER = 1, ST_IPM_MAXITER = 2, ST_PCG_MAXITER = 4, ST_PCG_BREAKDOWN = 8,
-              ST_NUMERIC = 16;
+              ST_NUMERIC = 16, ST_PCG_FLOOR = 32, ST_PCG_FALLBACK = 64;
 
 struct Params {
   int variant, precond;
@@ -43,7 +43,7 @@ struct DCode {
 // Byte offsets inside one warp's global slot and shared-memory window (host-computed).
 struct Layout {
   long long slot_bytes;
-  long long g_x, g_z, g_d2, g_v, g_y, g_dy, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
+  long long g_x, g_z, g_d2, g_v, g_y, g_dy, g_dyb, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
       g_offF, g_sgnC, g_mask, g_sgnV, g_flip;
   int smem_bytes;
   int s_keys;                                                                  // sort phase
@@ -87,7 +87,7 @@ struct Frame {
   const Layout* L;
   int lane;
   char* sm;
-  double *x, *z, *d2, *v, *y, *dy, *l, *w, *u, *b, *dinvF;
+  double *x, *z, *d2, *v, *y, *dy, *dyb, *l, *w, *u, *b, *dinvF;
   int *recB, *recF, *offB, *offF;
   uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
   uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
@@ -109,6 +109,7 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.v = (double*)(slot + L->g_v);
   F.y = (double*)(slot + L->g_y);
   F.dy = (double*)(slot + L->g_dy);
+  F.dyb = (double*)(slot + L->g_dyb);
   F.l = (double*)(slot + L->g_l);
   F.w = (double*)(slot + L->g_w);
   F.u = (double*)(slot + L->g_u);
@@ -602,6 +603,7 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 }
 
 // =====================================================================================
+// =====================================================================================
 // PCG (Alg. 4) on (A D^2 A^T) dy = w with x^0 = 0 (C-9), matrix-free:
 //   l = A (D^2 (A^T h)):  t_i = sum_j A_ji h_j (per variable), l_j = sum_i A_ji d2_i t_i
 //                         + d2_{n+j} h_j (per check)                   [eq.`Delta y` LHS]
@@ -609,7 +611,10 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 // Stops after line 9 once ||r||_2 <= tol ||w||_2 (G15).  h^T l <= 0 -> breakdown.
 // w is read from F.w; the solution accumulates in F.dy.
 // =====================================================================================
-__device__ __forceinline__ void precond_apply(const Frame& F, bool use_mtm, int nLb, int nLf,
+// Preconditioner modes of one PCG attempt.
+constexpr int PC_MTS = 0, PC_NONE = 1;
+
+__device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb, int nLf,
                                               double& rz) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
@@ -617,7 +622,7 @@ __device__ __forceinline__ void precond_apply(const Frame& F, bool use_mtm, int 
   double* fS = F.S<double>(L.s_f);
   double* zS = F.S<double>(L.s_z);
   double acc_rz = 0.0;
-  if (!use_mtm) {
+  if (mode != PC_MTS) {   // identity: plain CG
     for (int j = F.lane; j < C.m; j += 32) {
       double r = rS[j];
       zS[j] = r;
@@ -658,7 +663,8 @@ __device__ __forceinline__ void precond_apply(const Frame& F, bool use_mtm, int 
       }
       double zz = (head < 0) ? -acc : acc;
       zS[R] = zz;
-      acc_rz += zz * rS[R];
+      // z^T r = f^T D_M^-2 f (f = A_M^-1 r): a sum of squares, never <= 0 by cancellation
+      acc_rz += fS[R] * fS[R] * F.dinvF[s];
     }
     __syncwarp();
   }
@@ -670,102 +676,209 @@ struct PcgResult {
   double relres;
 };
 
-__device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, int nLb, int nLf) {
+// l = Q h = A (D^2 (A^T h)) matrix-free over the edges (eq.`Delta y` LHS), h in
+// shared memory (absent rows hold 0).  Returns h^T Q h accumulated as the sum of squares
+// sum_i d2_i (A^T h)_i^2 + sum_j d2_{n+j} h_j^2, so it is never <= 0 by cancellation.
+// With ABS, computes |A| D^2 |A|^T |h| instead (the rounding-floor estimate) and returns 0.
+template <bool ABS>
+__device__ __forceinline__ double spmv(const Frame& F) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  const double* hS = F.S<double>(L.s_h);
+  double* tS = F.S<double>(L.s_t);
+  double hl = 0.0;
+  for (int i = F.lane; i < C.n; i += 32) {
+    uint8_t s = F.sgnV[i];
+    if (!(s & 0xf)) continue;
+    int dv = C.var_deg[i];
+    double acc = 0.0;
+    for (int k = 0; k < dv; ++k) {
+      double hv = hS[var_ck(C, i, k)];
+      if (ABS) acc += fabs(hv);
+      else acc = ((s >> (4 + k)) & 1) ? acc - hv : acc + hv;
+    }
+    double tv = F.d2[i] * acc;
+    tS[i] = tv;
+    hl += acc * tv;
+  }
+  __syncwarp();
+  for (int j = F.lane; j < C.m; j += 32) {
+    uint16_t s = F.sgnC[j];
+    if (!(s & PRESENT)) continue;
+    int deg = C.chk_deg[j];
+    double hj = hS[j];
+    double ds = F.d2[C.n + j] * (ABS ? fabs(hj) : hj);
+    double acc = ds;
+    for (int t = 0; t < deg; ++t) {
+      double tv = tS[chk_nb(C, j, t)];
+      if (ABS) acc += tv;
+      else acc = ((s >> t) & 1) ? acc - tv : acc + tv;
+    }
+    F.l[j] = acc;
+    hl += hj * ds;
+  }
+  __syncwarp();
+  return ABS ? 0.0 : wsum(hl);
+}
+
+// One PCG run (Alg. 4) in preconditioner mode `mode`, from dy = 0, r = w.
+// The recursion stops after line 9 once ||r||_2 <= tol (G15); the TRUE residual w - Q dy is
+// then evaluated and must pass the same test.  Outcomes: 0 converged, ST_PCG_FLOOR (true
+// residual at the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||), ST_PCG_MAXITER,
+// ST_PCG_BREAKDOWN (h^T Q h or z^T r not > 0 / non-finite, the recursive residual
+// diverging 1e8-fold, or no new minimum in 200 iterations, or — MTS mode — a true residual
+// that fails the test after the recursion converged).  Non-MTS modes restart up to 4 times
+// from the true residual instead.  `it` accumulates iterations across runs.
+__device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int nLf, double wn,
+                       int& it, int cap, double& relres) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
   double* hS = F.S<double>(L.s_h);
   double* rS = F.S<double>(L.s_r);
+  const double tol = P.pcg_rel_tol * wn;
   double* zS = F.S<double>(L.s_z);
-  double* tS = F.S<double>(L.s_t);
   double* fS = F.S<double>(L.s_f);
-  // line 1-2: x^0 = 0, r^0 = w
-  double ww = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
     bool pr = (F.sgnC[j] & PRESENT) != 0;
-    double wj = pr ? F.w[j] : 0.0;
-    rS[j] = wj;
-    zS[j] = 0.0;
-    fS[j] = 0.0;
+    rS[j] = pr ? F.w[j] : 0.0;   // lines 1-2: x^0 = 0, r^0 = w
     F.dy[j] = 0.0;
-    ww += wj * wj;
+    zS[j] = 0.0;                 // absent rows stay exactly 0 in z, f and h (C-19)
+    fS[j] = 0.0;
   }
   __syncwarp();
-  double wn = sqrt(wsum(ww));
-  PcgResult res{0, 0, 0.0};
-  if (wn == 0.0) {
-    for (int j = F.lane; j < C.m; j += 32) hS[j] = 0.0;
+  relres = 1.0;
+  for (int restart = 0; restart <= 4; ++restart) {
+    double rz;
+    precond_apply(F, mode, nLb, nLf, rz);   // line 3
+    if (!(rz > 0.0) || !isfinite(rz)) return ST_PCG_BREAKDOWN;
+    for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? zS[j] : 0.0;   // line 4
     __syncwarp();
-    return res;
-  }
-  // line 3-4: z^0 = M^-1 r^0, h^0 = z^0
-  double rz;
-  precond_apply(F, use_mtm, nLb, nLf, rz);
-  for (int j = F.lane; j < C.m; j += 32) hS[j] = zS[j];
-  __syncwarp();
-  const double tol = P.pcg_rel_tol * wn;
-  res.status = ST_PCG_MAXITER;
-  res.relres = 1.0;
-  for (int it = 0; it < P.pcg_max_iter; ++it) {
-    // line 6: l = Q h (matrix-free)
-    for (int i = F.lane; i < C.n; i += 32) {
-      uint8_t s = F.sgnV[i];
-      if (!(s & 0xf)) continue;
-      int dv = C.var_deg[i];
-      double acc = 0.0;
-      for (int k = 0; k < dv; ++k) {
-        double hv = hS[var_ck(C, i, k)];  // absent rows hold h = 0
-        acc = ((s >> (4 + k)) & 1) ? acc - hv : acc + hv;
+    bool conv = false, bad = false;
+    double rrmin = 1e308;
+    int since_min = 0;
+    while (it < cap) {
+      double hl = spmv<false>(F);   // line 6: l = Q h
+      if (!(hl > 0.0) || !isfinite(hl)) {
+        bad = true;
+        break;
       }
-      tS[i] = F.d2[i] * acc;
+      const double alpha = rz / hl;   // line 7
+      double rr = 0.0;
+      for (int j = F.lane; j < C.m; j += 32) {
+        if (!(F.sgnC[j] & PRESENT)) continue;
+        F.dy[j] += alpha * hS[j];   // line 8
+        double r = rS[j] - alpha * F.l[j];   // line 9
+        rS[j] = r;
+        rr += r * r;
+      }
+      __syncwarp();
+      rr = wsum(rr);
+      ++it;
+      if (sqrt(rr) <= tol) {
+        conv = true;
+        break;
+      }
+      if (rr < rrmin) {
+        rrmin = rr;
+        since_min = 0;
+      } else if (mode == PC_MTS && (rr > 1e16 * rrmin || ++since_min > 200)) {
+        bad = true;
+        break;
+      }
+      double rz_new;
+      precond_apply(F, mode, nLb, nLf, rz_new);   // line 10
+      if (!(rz_new > 0.0) || !isfinite(rz_new)) {
+        bad = true;
+        break;
+      }
+      const double nu = rz_new / rz;   // line 11
+      rz = rz_new;
+      for (int j = F.lane; j < C.m; j += 32) {
+        if (!(F.sgnC[j] & PRESENT)) continue;
+        hS[j] = zS[j] + nu * hS[j];   // line 12
+      }
+      __syncwarp();
     }
+    if (bad) return ST_PCG_BREAKDOWN;
+    // true residual r = w - Q dy (h <- dy; h is rebuilt on restart)
+    for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
     __syncwarp();
-    double hl = 0.0;
-    for (int j = F.lane; j < C.m; j += 32) {
-      uint16_t s = F.sgnC[j];
-      if (!(s & PRESENT)) continue;
-      int deg = C.chk_deg[j];
-      double hj = hS[j];
-      double acc = F.d2[C.n + j] * hj;
-      for (int t = 0; t < deg; ++t) {
-        double tv = tS[chk_nb(C, j, t)];
-        acc = ((s >> t) & 1) ? acc - tv : acc + tv;
-      }
-      F.l[j] = acc;
-      hl += hj * acc;
-    }
-    hl = wsum(hl);
-    if (!(hl > 0.0) || !isfinite(hl)) {
-      res.status = ST_PCG_BREAKDOWN;
-      break;
-    }
-    // lines 7-9
-    double alpha = rz / hl;
+    spmv<false>(F);
     double rr = 0.0;
     for (int j = F.lane; j < C.m; j += 32) {
-      if (!(F.sgnC[j] & PRESENT)) continue;
-      F.dy[j] += alpha * hS[j];
-      double r = rS[j] - alpha * F.l[j];
+      double r = 0.0;
+      if (F.sgnC[j] & PRESENT) r = F.w[j] - F.l[j];
       rS[j] = r;
       rr += r * r;
     }
     __syncwarp();
-    rr = wsum(rr);
-    res.iters = it + 1;
-    res.relres = sqrt(rr) / wn;
-    if (sqrt(rr) <= tol) {
-      res.status = 0;
-      break;
-    }
-    // lines 10-12
-    double rz_new;
-    precond_apply(F, use_mtm, nLb, nLf, rz_new);
-    double nu = rz_new / rz;
-    rz = rz_new;
-    for (int j = F.lane; j < C.m; j += 32) {
-      if (!(F.sgnC[j] & PRESENT)) continue;
-      hS[j] = zS[j] + nu * hS[j];
-    }
+    const double trn = sqrt(wsum(rr));
+    relres = trn / wn;
+    if (!isfinite(trn)) return ST_PCG_BREAKDOWN;
+    if (trn <= tol) return 0;
+    // attainable-accuracy floor of the residual evaluation itself
+    spmv<true>(F);
+    double aa = 0.0;
+    for (int j = F.lane; j < C.m; j += 32)
+      if (F.sgnC[j] & PRESENT) aa += F.l[j] * F.l[j];
+    aa = sqrt(wsum(aa));
+    if (trn <= 16.0 * 2.220446049250313e-16 * aa) return ST_PCG_FLOOR;
+    if (!conv) return ST_PCG_MAXITER;
+    if (mode == PC_MTS) return ST_PCG_BREAKDOWN;   // recursion and truth disagree
+  }
+  return ST_PCG_MAXITER;
+}
+
+// Step solve of eq.`Delta y` by PCG.  precond = 0: the paper's column-wise MTS
+// preconditioner (Alg. 7).  Late in the IPM the column-wise set need not contain the
+// basic columns (Remark P:807-810); kappa(M^-1 Q) then explodes and the fp64 recursion
+// decouples from the true residual.  So (R-2): an MTS run that breaks down,
+// stalls, or whose TRUE residual is above tol (a floor-limited result above 1e-6 ||w||
+// included) is followed by a plain-CG run from dy = 0 (ST_PCG_FALLBACK,
+// informational), and the better of the two results is kept.  precond = 1: plain CG only.
+// w is read from F.w; the solution is left in F.dy.
+__device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, int nLb, int nLf) {
+  const DCode& C = *F.C;
+  double ww = 0.0;
+  for (int j = F.lane; j < C.m; j += 32) {
+    double wj = (F.sgnC[j] & PRESENT) ? F.w[j] : 0.0;
+    ww += wj * wj;
+    F.dy[j] = 0.0;
+  }
+  __syncwarp();
+  const double wn = sqrt(wsum(ww));
+  PcgResult res{0, 0, 0.0};
+  if (wn == 0.0) return res;
+  int it = 0;
+  if (!use_mtm) {
+    res.status = pcg_run(F, P, PC_NONE, 0, 0, wn, it, P.pcg_max_iter, res.relres);
+    res.iters = it;
+    return res;
+  }
+  double rel1 = 1.0;
+  int st1 = pcg_run(F, P, PC_MTS, nLb, nLf, wn, it, P.pcg_max_iter, rel1);
+  if (st1 == 0 || (st1 == ST_PCG_FLOOR && rel1 <= 1e-6)) {
+    res.status = st1;
+    res.relres = rel1;
+    res.iters = it;
+    return res;
+  }
+  const bool keep1 = (st1 == ST_PCG_FLOOR);   // a usable floor-limited MTS result
+  if (keep1)
+    for (int j = F.lane; j < C.m; j += 32) F.dyb[j] = F.dy[j];
+  __syncwarp();
+  int it2 = 0;
+  double rel2 = 1.0;
+  int st2 = pcg_run(F, P, PC_NONE, 0, 0, wn, it2, P.pcg_max_iter, rel2);
+  res.iters = it + it2;
+  if (keep1 && (st2 != 0) && !(st2 == ST_PCG_FLOOR && rel2 <= rel1)) {
+    for (int j = F.lane; j < C.m; j += 32) F.dy[j] = F.dyb[j];
     __syncwarp();
+    res.status = st1 | ST_PCG_FALLBACK;
+    res.relres = rel1;
+  } else {
+    res.status = st2 | ST_PCG_FALLBACK;
+    res.relres = rel2;
   }
   return res;
 }

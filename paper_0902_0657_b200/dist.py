@@ -1,0 +1,48 @@
+"""Frame sharding across ranks.
+
+Frames are independent LP-decoding problems, so the multi-GPU path has no data-path
+collective: global frame g belongs to rank g mod world_size (interleaved, which spreads
+the rare hard — fractional — frames evenly), each rank regenerates its own frames from
+the per-frame-keyed RNG, decodes them with one alp_decode call, and the run ends with
+one SUM all-reduce of the integer counters and one MAX all-reduce of the timed duration.
+Works on any torch.distributed backend (nccl on the GPU box, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+# order of the counter vector reduced at the end of a run
+COUNTERS = ("frames", "frame_errors", "not_certified", "lp_solves", "ipm_iters", "pcg_iters",
+            "status_nonzero", "pcg_bytes")
+
+
+def shard_frame_ids(frames_per_rank: int, rank: int, world_size: int) -> np.ndarray:
+    """Global frame ids owned by `rank` when every rank decodes frames_per_rank frames."""
+    if not (0 <= rank < world_size):
+        raise ValueError("rank out of range")
+    return np.arange(frames_per_rank, dtype=np.int64) * world_size + rank
+
+
+def frame_counters(hard, codewords, certificate, status, stats) -> np.ndarray:
+    """Per-rank counter vector (COUNTERS order) from one decode's host-side outputs."""
+    hard = np.asarray(hard)
+    errs = int(np.any(hard != np.asarray(codewords), axis=1).sum())
+    return np.array([hard.shape[0], errs, int((np.asarray(certificate) == 0).sum()),
+                     int(stats["lp_solves"].sum()), int(stats["ipm_iters"].sum()),
+                     int(stats["pcg_iters"].sum()), int((np.asarray(status) != 0).sum()),
+                     float(stats["pcg_bytes"].sum())], dtype=np.float64)
+
+
+def reduce_run(counters: np.ndarray, seconds: float, device=None) -> tuple[np.ndarray, float]:
+    """SUM of the counters and MAX of the timed duration over all ranks (identity when
+    torch.distributed is not initialised)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return np.asarray(counters, dtype=np.float64), float(seconds)
+    dev = device if device is not None else torch.device("cpu")
+    c = torch.tensor(np.asarray(counters, dtype=np.float64), device=dev)
+    t = torch.tensor([float(seconds)], dtype=torch.float64, device=dev)
+    dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return c.cpu().numpy(), float(t.item())

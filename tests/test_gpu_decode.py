@@ -62,7 +62,8 @@ def assert_certified(code, llr, g):
     cert = dual_certificate_batch(code, llr, g["u"], g["y"], g["masks"])
     bad = np.nonzero(~cert["ok"])[0]
     assert bad.size == 0, f"P6 certificate fails on frames {bad[:10]} (gap {cert['gap'][bad[:5]]})"
-    assert np.all(g["status"] == 0), np.unique(g["status"], return_counts=True)
+    # P4: no cap / breakdown / numeric bits (PCG_FLOOR = 32, PCG_FALLBACK = 64 are informational)
+    assert np.all((g["status"] & ~96) == 0), np.unique(g["status"], return_counts=True)
 
 
 def test_h7_golden_fractional_output():
@@ -83,9 +84,11 @@ def test_h1_examples_and_zero_lp_frames():
     llr = np.array([[-3.0, 1.0, 2.0, -1.0], [1.0, 1.0, 1.0, 1.0], [-1.0, -2.0, 3.0, 4.0]])
     out = gpu_decode(code, llr)
     np.testing.assert_allclose(out["u"][0], [1, 1, 0, 1], atol=1e-7)
-    assert list(out["cert"]) == [1, 1, 1]
+    assert list(out["cert"]) == [1, 1, 0]
     assert out["stats"]["lp_solves"][1] == 0 and out["obj"][1] == 0.0     # C-15
-    assert out["stats"]["lp_solves"][2] == 0 and out["obj"][2] == -3.0
+    # (1,1,0,0) violates check 1: two LPs end at the fractional (1, 1/2, 1/2, 0), objective -1/2
+    np.testing.assert_allclose(out["u"][2], [1, 0.5, 0.5, 0], atol=1e-7)
+    assert out["stats"]["lp_solves"][2] == 2 and abs(out["obj"][2] + 0.5) <= 1e-6
 
 
 @pytest.mark.parametrize("variant", ["A", "B"])

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 from scipy.optimize import linprog
 
-from oracle.lp import (newton_direction, step_lengths, ipm_solve, cholesky_solve,
+from oracle.lp import (newton_direction, step_lengths, ipm_solve, cholesky_solve, step_solve_exact,
                        normal_matrix, augmented_lp, DEFAULT_PARAMS, find_violated_cut)
 from synth.codes import regular_code
 
@@ -117,3 +117,52 @@ def test_empty_pool_lp_optimum_is_zero():
     res = ipm_solve(A, np.zeros(0), np.array([1.0, 2.0, 3.0]))
     assert res["status"] == 0
     assert np.max(res["x"]) < 1e-8
+
+
+def _exact_rational_solve(A, d2, w):
+    """Gauss-Jordan over the rationals (fractions.Fraction): the exact solution."""
+    from fractions import Fraction as Fr
+    p, q = A.shape
+    d2f = [Fr(float(v)) for v in d2]
+    Q = [[sum(Fr(int(A[a, i])) * d2f[i] * Fr(int(A[b, i])) for i in range(q) if A[a, i] and A[b, i])
+          for b in range(p)] for a in range(p)]
+    M = [Q[a] + [Fr(float(w[a]))] for a in range(p)]
+    for k in range(p):
+        piv = next(r for r in range(k, p) if M[r][k] != 0)
+        M[k], M[piv] = M[piv], M[k]
+        for r in range(p):
+            if r != k and M[r][k] != 0:
+                f = M[r][k] / M[k][k]
+                M[r] = [a - f * b for a, b in zip(M[r], M[k])]
+    return np.array([float(M[k][p] / M[k][k]) for k in range(p)])
+
+
+@pytest.mark.parametrize("seed,span", [(0, 2), (1, 8), (2, 14)])
+def test_step_solve_exact_matches_rational_solution(seed, span):
+    """Pin: on small config-5-like systems (one random odd cut per check, slack columns, d^2
+    log-uniform over span decades, kappa up to ~1e15) the extended-precision solve equals
+    the exact rational solution to 1e-10 relative (observed <= 6e-12 at kappa 1e10, where
+    fp64 Cholesky is off by ~4e-9)."""
+    from synth import c5_systems
+    from tests.helpers import dense_step_matrix, step_weights
+    code = regular_code(24, 3, 6, seed=10 + seed)
+    sy = c5_systems([seed], code, lo=-span / 2, hi=span / 2)
+    A, rows = dense_step_matrix(code, sy.masks[0])
+    d2 = step_weights(code, sy.d[0], rows)
+    w = sy.r[0][rows]
+    exact = _exact_rational_solve(A, d2, w)
+    got = step_solve_exact(A, d2, w)
+    assert np.linalg.norm(got - exact) <= 1e-10 * np.linalg.norm(exact)
+
+
+def test_step_solve_exact_agrees_with_lapack_when_well_conditioned():
+    rng = np.random.default_rng(5)
+    code = regular_code(60, 3, 6, seed=3)
+    from synth import c5_systems
+    from tests.helpers import dense_step_matrix, step_weights
+    sy = c5_systems([7], code, lo=-0.5, hi=0.5)
+    A, rows = dense_step_matrix(code, sy.masks[0])
+    d2 = step_weights(code, sy.d[0], rows)
+    w = rng.normal(size=len(rows))
+    np.testing.assert_allclose(step_solve_exact(A, d2, w), np.linalg.solve(normal_matrix(A, d2), w),
+                               rtol=1e-12)
