@@ -67,7 +67,9 @@ typedef enum {
 /* Per-frame status bits (values, not errors). */
 typedef enum {
   ALP_FRAME_OK = 0,
-  ALP_FRAME_ALP_MAXITER = 1,     /* alp_max_iter LPs solved and cuts still change (C-12)   */
+  ALP_FRAME_ALP_MAXITER = 1,     /* alp_max_iter LPs solved and cuts still change, or the cut
+                                    pool repeated that of an LP already solved (a
+                                    deterministic MALP cycle; C-12)                        */
   ALP_FRAME_IPM_MAXITER = 2,     /* some LP hit ipm_max_iter Newton steps                   */
   ALP_FRAME_PCG_MAXITER = 4,     /* some PCG solve ended above pcg_rel_tol at pcg_max_iter  */
   ALP_FRAME_PCG_BREAKDOWN = 8,   /* some PCG solve met h^T Q h <= 0 (or non-finite)          */
@@ -77,12 +79,16 @@ typedef enum {
                                     16 eps || |A| D^2 |A|^T |dy| ||_2, above pcg_rel_tol ||w|| */
   ALP_FRAME_PCG_FALLBACK = 64    /* informational: some MTS-preconditioned PCG run broke down
                                     or failed the true-residual test, and the solve was redone
-                                    by plain CG; the better result was kept (R-2) */
+                                    by Jacobi-preconditioned CG; the better result was kept
+                                    (R-2)                                         */
 } alp_frame_status;
 
 typedef struct alp_code alp_code;   /* opaque, immutable after creation */
 
-/* Per-frame counters (alp_decode) — 32 bytes. */
+/* Per-frame counters (alp_decode) — 80 bytes.  cyc_* are SM clock cycles (clock64) the
+ * frame's warp spent per phase: cut search + sign tables, IPM body (residuals, rhs,
+ * Newton recovery, update), preconditioner build (sort, Alg. 7 peel, level schedule),
+ * PCG SpMV, PCG preconditioner sweeps, remaining PCG work (axpys, dots, true residual). */
 typedef struct {
   int32_t lp_solves;   /* LPs solved (MALP outer iterations that added a cut)            */
   int32_t ipm_iters;   /* Newton steps summed over all LPs                                */
@@ -90,6 +96,7 @@ typedef struct {
   int32_t max_p;       /* largest number of LP rows p (<= m, Cor. 3 P:289-292)             */
   double g_max;        /* max_i min(u_i, 1 - u_i) of the output (integrality, C-11)       */
   double pcg_bytes;    /* sum over PCG iterations of B_min(p, n_act, m)    */
+  int64_t cyc_cut, cyc_ipm, cyc_build, cyc_spmv, cyc_sweep, cyc_pcg_other;
 } alp_frame_stats;
 
 typedef struct {
@@ -102,10 +109,12 @@ typedef struct {
   double pcg_rel_tol;     /* PCG stop: ||r||_2 <= pcg_rel_tol * ||w||_2 (C-9, G15) on the
                              recursive residual, then verified on the TRUE residual
                              w - Q dy (restart from it if needed; R-1)      1e-8   */
+  double pcg_fallback_tol;/* relative true-residual target of the Jacobi-CG fallback run
+                             (R-2)                                          1e-8   */
   double tau_viol;        /* cut violated iff lhs < 1 - tau_viol (C-3)                  1e-6   */
   double tau_act;         /* cut active iff slack <= tau_act (C-4)                      1e-6   */
   double tau_cert;        /* certificate needs g_max <= tau_cert (C-11)                 1e-2   */
-  int32_t alp_max_iter;   /* LP cap per frame (C-12)                                    200    */
+  int32_t alp_max_iter;   /* LP cap per frame (C-12), <= 255                            200    */
   int32_t ipm_max_iter;   /* Newton steps per LP (C-8)                                  100    */
   int32_t pcg_max_iter;   /* PCG iterations per Newton step (C-9)                       1000   */
   int32_t warps_per_block;/* tuning: frames (one warp each) per CTA; 0 = automatic             */
@@ -177,6 +186,12 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
                         int32_t* pcg_iters, double* rel_res, int32_t* sys_status,
                         int32_t* pivot_rows, int32_t* pivot_cols, void* workspace,
                         size_t workspace_bytes, const alp_params* params, void* stream);
+
+/* Diagnostics: when `records` (DEVICE, capacity x 80-byte records {int32 frame, lp, ipm_it,
+ * p, status, pcg_iters; fp64 relres, d2_min, d2_max, mu, ||r_b||inf, ||r_c||inf, gap}) is non-NULL, every subsequent
+ * alp_decode appends one record per Newton-step solve (order unspecified, records beyond
+ * capacity dropped).  NULL disables.  Process-wide; not thread safe; not for production. */
+alp_status alp_debug_trace(void* records, int32_t capacity);
 
 /* Kernel launches enqueued by the last successful alp_decode / ipm_step_pcg on this thread. */
 int32_t alp_last_launch_count(void);

@@ -329,7 +329,9 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
     variant "B": MALP-B: first remove every inactive pool cut, then as "A".
     variant "ALP": Alg. 1: add every violated cut found at u^{k-1}; never
       remove (several cuts per check may accumulate).
-    At most alp_max_iter LPs (C-12); a frame that would need more gets ST_ALP_MAXITER.
+    At most alp_max_iter LPs (C-12); a frame that would need more gets ST_ALP_MAXITER, and
+    so does a MALP frame whose new pool equals the pool of an LP it already solved (the
+    deterministic cycle C-12 describes; detected before solving the repeat).
     """
     P = dict(DEFAULT_PARAMS) if params is None else params
     gamma = np.asarray(gamma, dtype=np.float64)
@@ -342,6 +344,7 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
     y_check = np.zeros(m)
     trace = []
     objs = []
+    seen_pools = set()      # reading C-12: a repeated pool is a deterministic cycle
     for k in range(P["alp_max_iter"] + 1):
         changed = False
         if variant == "B":
@@ -363,6 +366,15 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
         if k == P["alp_max_iter"]:
             status |= ST_ALP_MAXITER
             break
+        if variant != "ALP":
+            # The LP, hence u^k and the next cut search, are functions of the pool alone:
+            # a pool equal to an earlier LP's pool repeats forever (C-12).  Stop with the
+            # last solved u (G2) and the cap status.
+            key = frozenset((j, int(mask_word(v))) for j, v in pool.items())
+            if key in seen_pools:
+                status |= ST_ALP_MAXITER
+                break
+            seen_pools.add(key)
         if variant == "ALP":
             lp = _augmented_multi(code, alp_rows, gamma)
         else:

@@ -13,6 +13,7 @@ class AlpParams(C.Structure):
         ("variant", C.c_int32), ("precond", C.c_int32),
         ("sigma", C.c_double), ("eta", C.c_double),
         ("gap_tol", C.c_double), ("feas_tol", C.c_double), ("pcg_rel_tol", C.c_double),
+        ("pcg_fallback_tol", C.c_double),
         ("tau_viol", C.c_double), ("tau_act", C.c_double), ("tau_cert", C.c_double),
         ("alp_max_iter", C.c_int32), ("ipm_max_iter", C.c_int32), ("pcg_max_iter", C.c_int32),
         ("warps_per_block", C.c_int32),
@@ -23,12 +24,17 @@ class FrameStats(C.Structure):
     _fields_ = [
         ("lp_solves", C.c_int32), ("ipm_iters", C.c_int32), ("pcg_iters", C.c_int32),
         ("max_p", C.c_int32), ("g_max", C.c_double), ("pcg_bytes", C.c_double),
+        ("cyc_cut", C.c_int64), ("cyc_ipm", C.c_int64), ("cyc_build", C.c_int64),
+        ("cyc_spmv", C.c_int64), ("cyc_sweep", C.c_int64), ("cyc_pcg_other", C.c_int64),
     ]
 
 
-# numpy dtype of alp_frame_stats (32 bytes) for zero-copy views of device/host buffers
+# numpy dtype of alp_frame_stats (80 bytes) for zero-copy views of device/host buffers
 STATS_FIELDS = [("lp_solves", "<i4"), ("ipm_iters", "<i4"), ("pcg_iters", "<i4"),
-                ("max_p", "<i4"), ("g_max", "<f8"), ("pcg_bytes", "<f8")]
+                ("max_p", "<i4"), ("g_max", "<f8"), ("pcg_bytes", "<f8"),
+                ("cyc_cut", "<i8"), ("cyc_ipm", "<i8"), ("cyc_build", "<i8"),
+                ("cyc_spmv", "<i8"), ("cyc_sweep", "<i8"), ("cyc_pcg_other", "<i8")]
+STATS_BYTES = 80
 
 P = C.c_void_p
 SIGNATURES = {
@@ -45,6 +51,7 @@ SIGNATURES = {
     "ipm_step_pcg": (C.c_int, [P, C.c_int64, P, P, P, P, P, P, P, P, P, P, P, C.c_size_t,
                                C.POINTER(AlpParams), P]),
     "alp_last_launch_count": (C.c_int32, []),
+    "alp_debug_trace": (C.c_int, [P, C.c_int32]),
     "alp_status_string": (C.c_char_p, [C.c_int]),
     "alp_last_error": (C.c_char_p, []),
     "alp_build_info": (C.c_char_p, []),

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _ffi
-from ._ffi import AlpParams, STATS_FIELDS
+from ._ffi import AlpParams, STATS_FIELDS, STATS_BYTES
 
 STATUS_NAMES = {0: "ALP_OK", -1: "ALP_ERR_INVALID_ARG", -2: "ALP_ERR_BAD_CODE",
                 -3: "ALP_ERR_UNSUPPORTED", -4: "ALP_ERR_CUDA", -5: "ALP_ERR_WORKSPACE"}
@@ -114,7 +114,7 @@ class DecodeResult:
     objective: torch.Tensor   # [F] float64
     certificate: torch.Tensor  # [F] uint8
     status: torch.Tensor      # [F] int32
-    stats: torch.Tensor       # [F, 32] uint8 (alp_frame_stats); see stats_numpy()
+    stats: torch.Tensor       # [F, 80] uint8 (alp_frame_stats); see stats_numpy()
     u: torch.Tensor | None = None
     y: torch.Tensor | None = None
     masks: torch.Tensor | None = None
@@ -138,7 +138,7 @@ def decode(code: Code, llr: torch.Tensor, params: AlpParams | None = None, want_
             objective=torch.empty(F, dtype=torch.float64, device=dev),
             certificate=torch.empty(F, dtype=torch.uint8, device=dev),
             status=torch.empty(F, dtype=torch.int32, device=dev),
-            stats=torch.empty((F, 32), dtype=torch.uint8, device=dev),
+            stats=torch.empty((F, STATS_BYTES), dtype=torch.uint8, device=dev),
             u=torch.empty((F, code.n), dtype=torch.float64, device=dev) if want_u else None,
             y=torch.empty((F, code.m), dtype=torch.float64, device=dev) if want_y else None,
             masks=torch.empty((F, code.m), dtype=torch.int16, device=dev) if want_masks else None,

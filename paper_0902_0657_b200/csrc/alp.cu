@@ -15,6 +15,15 @@
 
 namespace alp {
 
+// Optional per-Newton-step trace (alp_debug_trace): one record per step solve.
+struct TraceRec {
+  int frame, lp, ipm_it, p, status, iters;
+  double relres, d2min, d2max, mu, rb, rc, gap;
+};
+__device__ TraceRec* g_trace = nullptr;
+__device__ int g_trace_cap = 0;
+__device__ int g_trace_n = 0;
+
 struct IpmOut {
   int iters, status, pcg_iters;
   double pcg_bytes;
@@ -32,7 +41,7 @@ struct IpmOut {
 // then the PCG right-hand side.
 // =====================================================================================
 __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
-                            double bmax, double cmax) {
+                            double bmax, double cmax, long long frame_id, int lp_id) {
   const DCode& C = *F.C;
   const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
   const double q = (double)(n + p);
@@ -45,6 +54,7 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
   for (int j = lane; j < m; j += 32) F.y[j] = 0.0;
   __syncwarp();
   IpmOut out{0, 0, 0, 0.0};
+  long long tk = clock64();
   // algorithmic bytes per PCG iteration of this LP
   const double Bmin = 8.0 * (nact + p) + 48.0 * p + 5.0 * p + 2.0 * m;
   int it = 0;
@@ -118,9 +128,32 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
     __syncwarp();
     int nLb = 0, nLf = 0;
     const bool mtm = (P.precond == 0);
+    ALP_TICK(F, CY_IPM, tk);
     if (mtm) build_precond(F, p, nLb, nLf);
-    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf);
+    ALP_TICK(F, CY_BUILD, tk);
+    // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to
+    // well below z ~ mu on the basic columns, so late in the IPM the recursion runs to
+    // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); acceptance stays ||w - Q dy|| <= 1e-8||w||
+    const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, 1e-2 * mu));
+    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, inner);
+    tk = clock64();
+
     out.status |= pr.status;
+    if (g_trace) {
+      double dmn = 1e308, dmx = 0.0;
+      for (int c = lane; c < Q; c += 32) {
+        if (c >= n && !(F.sgnC[c - n] & PRESENT)) continue;
+        dmn = fmin(dmn, F.d2[c]);
+        dmx = fmax(dmx, F.d2[c]);
+      }
+      dmn = wmin(dmn);
+      dmx = wmax(dmx);
+      if (lane == 0) {
+        int slot = atomicAdd(&g_trace_n, 1);
+        if (slot < g_trace_cap)
+          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, pr.relres, dmn, dmx, mu, rbn, rcn, gap};
+      }
+    }
     out.pcg_iters += pr.iters;
     out.pcg_bytes += (double)pr.iters * Bmin;
     double ax = 1e308, az = 1e308;
@@ -181,6 +214,7 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
       break;
     }
   }
+  ALP_TICK(F, CY_IPM, tk);
   out.iters = it;
   return out;
 }
@@ -217,6 +251,9 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   __syncwarp();
   int status = 0, lp_solves = 0, ipm_iters = 0, pcg_iters = 0, max_p = 0;
   double pcg_bytes = 0.0;
+  if (lane < 8) F.cyc[lane] = 0;
+  __syncwarp();
+  long long tk = clock64();
   for (int k = 0;; ++k) {
     bool changed = cut_search(F, P);
     if (!changed) break;
@@ -224,12 +261,37 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
       status |= ST_ALP_MAXITER;
       break;
     }
+    // Reading C-12: the LP (hence u^k and the next cut search) is a function of the pool, so
+    // a pool equal to that of an LP already solved repeats forever: stop with the last solved
+    // u (G2) and the cap status.  Pools are compared by a 64-bit order-independent hash.
+    {
+      unsigned long long hsh = 0ull;
+      for (int j = lane; j < m; j += 32) {
+        unsigned long long v = ((unsigned long long)(unsigned)j << 16) | F.mask[j];
+        v *= 0x9E3779B97F4A7C15ull;
+        v ^= v >> 29;
+        v *= 0xBF58476D1CE4E5B9ull;
+        v ^= v >> 32;
+        hsh += (F.mask[j] & PRESENT) ? v : 0ull;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) hsh += __shfl_xor_sync(FULL, hsh, o);
+      bool seen = false;
+      for (int t = lane; t < k; t += 32) seen |= (F.hist[t] == hsh);
+      if (__any_sync(FULL, seen)) {
+        status |= ST_ALP_MAXITER;
+        break;
+      }
+      if (lane == 0) F.hist[k] = hsh;
+      __syncwarp();
+    }
     int p, nact;
     double bmax;
     build_signs(F, true, p, nact, bmax);
+    ALP_TICK(F, CY_CUT, tk);
     ++lp_solves;
     max_p = max(max_p, p);
-    IpmOut o = ipm_solve(F, P, g, p, nact, bmax, cmax);
+    IpmOut o = ipm_solve(F, P, g, p, nact, bmax, cmax, f, lp_solves);
     status |= o.status;
     ipm_iters += o.iters;
     pcg_iters += o.pcg_iters;
@@ -239,8 +301,10 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
       F.u[i] = F.flip[i] ? 1.0 - xi : xi;
     }
     __syncwarp();
+    tk = clock64();
     if (o.status & ST_NUMERIC) break;
   }
+  ALP_TICK(F, CY_CUT, tk);
   // outputs: hard decision, objective gamma^T u, g_max, ML certificate
   double obj = 0.0, gm = 0.0;
   for (int i = lane; i < n; i += 32) {
@@ -275,6 +339,12 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
       st.max_p = max_p;
       st.g_max = gm;
       st.pcg_bytes = pcg_bytes;
+      st.cyc_cut = F.cyc[CY_CUT];
+      st.cyc_ipm = F.cyc[CY_IPM];
+      st.cyc_build = F.cyc[CY_BUILD];
+      st.cyc_spmv = F.cyc[CY_SPMV];
+      st.cyc_sweep = F.cyc[CY_SWEEP];
+      st.cyc_pcg_other = F.cyc[CY_PCG];
       O.stats[f] = st;
     }
   }
@@ -349,7 +419,7 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
           if (io.pcol) io.pcol[s * m + k] = -1;
         }
     }
-    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf);
+    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, P.pcg_rel_tol);
     for (int j = lane; j < m; j += 32) io.dy[s * m + j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
     if (lane == 0) {
       if (io.iters) io.iters[s] = pr.iters;
@@ -421,6 +491,7 @@ Layout make_layout(const DCode& C) {
     o += al(bytes, 128);
     return (long long)r;
   };
+  L.g_cyc = g(8 * 8);
   L.g_x = g(8 * Q);
   L.g_z = g(8 * Q);
   L.g_d2 = g(8 * Q);
@@ -439,6 +510,8 @@ Layout make_layout(const DCode& C) {
   L.g_offF = g(4 * (m + 2));
   L.g_sgnC = g(2 * m);
   L.g_mask = g(2 * m);
+  L.g_hist = g(8 * 256);
+  L.g_prc = g(2 * Q);
   L.g_sgnV = g(n);
   L.g_flip = g(n);
   L.slot_bytes = (long long)al(o, 256);
@@ -503,6 +576,7 @@ Params make_params(const alp_params* p) {
   P.gap_tol = p->gap_tol;
   P.feas_tol = p->feas_tol;
   P.pcg_rel_tol = p->pcg_rel_tol;
+  P.pcg_fallback_tol = p->pcg_fallback_tol;
   P.tau_viol = p->tau_viol;
   P.tau_act = p->tau_act;
   P.tau_cert = p->tau_cert;
@@ -518,8 +592,8 @@ alp_status check_params(const alp_params* p) {
   if (p->precond < 0 || p->precond > 1) return fail(ALP_ERR_INVALID_ARG, "params.precond must be 0 or 1");
   if (!(p->sigma > 0 && p->sigma < 1) || !(p->eta > 0 && p->eta < 1))
     return fail(ALP_ERR_INVALID_ARG, "params.sigma and params.eta must lie in (0,1)");
-  if (p->alp_max_iter < 0 || p->ipm_max_iter < 0 || p->pcg_max_iter < 1)
-    return fail(ALP_ERR_INVALID_ARG, "iteration caps must be non-negative (pcg >= 1)");
+  if (p->alp_max_iter < 0 || p->alp_max_iter > 255 || p->ipm_max_iter < 0 || p->pcg_max_iter < 1)
+    return fail(ALP_ERR_INVALID_ARG, "iteration caps: 0 <= alp_max_iter <= 255, ipm >= 0, pcg >= 1");
   if (p->warps_per_block < 0 || p->warps_per_block > 4)
     return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..4");
   return ALP_OK;
@@ -576,6 +650,7 @@ void alp_default_params(alp_params* p) {
   p->gap_tol = 1e-9;
   p->feas_tol = 1e-8;
   p->pcg_rel_tol = 1e-8;
+  p->pcg_fallback_tol = 1e-8;
   p->tau_viol = 1e-6;
   p->tau_act = 1e-6;
   p->tau_cert = 1e-2;
@@ -604,6 +679,15 @@ const char* alp_build_info(void) {
 }
 
 int32_t alp_last_launch_count(void) { return g_last_launches; }
+
+alp_status alp_debug_trace(void* records, int32_t capacity) {
+  void* ptr = records;
+  int cap = records ? capacity : 0, zero = 0;
+  cudaError_t e = cudaMemcpyToSymbol(g_trace, &ptr, sizeof(ptr));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
+  return e == cudaSuccess ? ALP_OK : cuda_fail(e, "alp_debug_trace");
+}
 
 alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const int32_t* col_idx,
                            alp_code** out) {

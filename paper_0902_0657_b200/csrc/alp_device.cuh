@@ -26,7 +26,7 @@ constexpr int ST_ALP_MAXITER = 1, ST_IPM_MAXITER = 2, ST_PCG_MAXITER = 4, ST_PCG
 
 struct Params {
   int variant, precond;
-  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, tau_viol, tau_act, tau_cert;
+  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, pcg_fallback_tol, tau_viol, tau_act, tau_cert;
   int alp_max_iter, ipm_max_iter, pcg_max_iter;
 };
 
@@ -43,8 +43,8 @@ struct DCode {
 // Byte offsets inside one warp's global slot and shared-memory window (host-computed).
 struct Layout {
   long long slot_bytes;
-  long long g_x, g_z, g_d2, g_v, g_y, g_dy, g_dyb, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
-      g_offF, g_sgnC, g_mask, g_sgnV, g_flip;
+  long long g_cyc, g_x, g_z, g_d2, g_v, g_y, g_dy, g_dyb, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
+      g_offF, g_sgnC, g_mask, g_hist, g_prc, g_sgnV, g_flip;
   int smem_bytes;
   int s_keys;                                                                  // sort phase
   int s_order, s_rank, s_cnt, s_xr, s_bm, s_pos, s_pcol, s_prow, s_lvB, s_lvF;  // peel phase
@@ -81,6 +81,15 @@ __device__ __forceinline__ int wmaxi(int v) {
   return v;
 }
 
+// Phase clock: lane 0 adds the cycles since `t` to counter `ph` and restarts `t`.
+enum { CY_CUT = 0, CY_IPM = 1, CY_BUILD = 2, CY_SPMV = 3, CY_SWEEP = 4, CY_PCG = 5 };
+#define ALP_TICK(F, ph, t)                          \
+  do {                                              \
+    long long now_ = clock64();                     \
+    if ((F).lane == 0) (F).cyc[ph] += now_ - (t);   \
+    (t) = now_;                                     \
+  } while (0)
+
 // Per-frame working set: pointers into the warp's global slot and shared window.
 struct Frame {
   const DCode* C;
@@ -91,8 +100,11 @@ struct Frame {
   int *recB, *recF, *offB, *offF;
   uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
   uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
+  unsigned long long* hist;  // [alp_max_iter + 1] pool hashes of the LPs solved (C-12)
+  uint16_t* prc;   // [q]: pivot row of each column of the MTS set, NONE16 if not a pivot
   uint8_t* sgnV;   // [n]: bit k <-> k-th check of the variable present; bit 4+k <-> coef -1
   uint8_t* flip;   // [n]: 1 <-> gamma_i < 0 (x_i = 1 - u_i, §IV-B)
+  long long* cyc;  // [8] per-phase clock64 accumulators (lane 0 writes; alp_frame_stats)
   template <class T>
   __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(sm + off); }
 };
@@ -103,6 +115,7 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.L = L;
   F.lane = lane;
   F.sm = sm;
+  F.cyc = (long long*)(slot + L->g_cyc);
   F.x = (double*)(slot + L->g_x);
   F.z = (double*)(slot + L->g_z);
   F.d2 = (double*)(slot + L->g_d2);
@@ -121,6 +134,8 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.offF = (int*)(slot + L->g_offF);
   F.sgnC = (uint16_t*)(slot + L->g_sgnC);
   F.mask = (uint16_t*)(slot + L->g_mask);
+  F.prc = (uint16_t*)(slot + L->g_prc);
+  F.hist = (unsigned long long*)(slot + L->g_hist);
   F.sgnV = (uint8_t*)(slot + L->g_sgnV);
   F.flip = (uint8_t*)(slot + L->g_flip);
 }
@@ -566,6 +581,7 @@ __device__ void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
     poc[pcol[R]] = (uint16_t)R;
   }
   __syncwarp();
+  for (int c = F.lane; c < C.Q; c += 32) F.prc[c] = poc[c];
   uint16_t* lvB = F.S<uint16_t>(L.s_lvB);
   uint16_t* lvF = F.S<uint16_t>(L.s_lvF);
   nLb = compute_levels<false>(F, p, lvB);
@@ -611,27 +627,13 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 // Stops after line 9 once ||r||_2 <= tol ||w||_2 (G15).  h^T l <= 0 -> breakdown.
 // w is read from F.w; the solution accumulates in F.dy.
 // =====================================================================================
-// Preconditioner modes of one PCG attempt.
-constexpr int PC_MTS = 0, PC_NONE = 1;
-
-__device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb, int nLf,
-                                              double& rz) {
+// Back substitution A_M f = r over the level schedule (P:585 stage 1): r in s_r, f in s_f,
+// both indexed by pivot row; f_R is the component of row R's pivot column.
+__device__ __forceinline__ void back_sweep(const Frame& F, int nLb) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
-  double* rS = F.S<double>(L.s_r);
+  const double* rS = F.S<double>(L.s_r);
   double* fS = F.S<double>(L.s_f);
-  double* zS = F.S<double>(L.s_z);
-  double acc_rz = 0.0;
-  if (mode != PC_MTS) {   // identity: plain CG
-    for (int j = F.lane; j < C.m; j += 32) {
-      double r = rS[j];
-      zS[j] = r;
-      acc_rz += r * r;
-    }
-    __syncwarp();
-    rz = wsum(acc_rz);
-    return;
-  }
   const int RB = C.RB;
   for (int lvl = 0; lvl < nLb; ++lvl) {
     int s0 = F.offB[lvl], s1 = F.offB[lvl + 1];
@@ -649,6 +651,31 @@ __device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb,
     }
     __syncwarp();
   }
+}
+
+// Preconditioner modes of one PCG attempt.
+constexpr int PC_MTS = 0, PC_NONE = 1, PC_JACOBI = 2;
+
+__device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb, int nLf,
+                                              double& rz) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  double* rS = F.S<double>(L.s_r);
+  double* fS = F.S<double>(L.s_f);
+  double* zS = F.S<double>(L.s_z);
+  double acc_rz = 0.0;
+  if (mode != PC_MTS) {   // identity (plain CG) or Jacobi z = r / diag(Q) (dinvF)
+    for (int j = F.lane; j < C.m; j += 32) {
+      double r = rS[j];
+      double z = (mode == PC_JACOBI) ? r * F.dinvF[j] : r;
+      zS[j] = z;
+      acc_rz += r * z;   // sum of r_j^2 / Q_jj >= 0
+    }
+    __syncwarp();
+    rz = wsum(acc_rz);
+    return;
+  }
+  back_sweep(F, nLb);
   for (int lvl = 0; lvl < nLf; ++lvl) {
     int s0 = F.offF[lvl], s1 = F.offF[lvl + 1];
     for (int s = s0 + F.lane; s < s1; s += 32) {
@@ -726,16 +753,18 @@ __device__ __forceinline__ double spmv(const Frame& F) {
 // then evaluated and must pass the same test.  Outcomes: 0 converged, ST_PCG_FLOOR (true
 // residual at the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||), ST_PCG_MAXITER,
 // ST_PCG_BREAKDOWN (h^T Q h or z^T r not > 0 / non-finite, the recursive residual
-// diverging 1e8-fold, or no new minimum in 200 iterations, or — MTS mode — a true residual
-// that fails the test after the recursion converged).  Non-MTS modes restart up to 4 times
-// from the true residual instead.  `it` accumulates iterations across runs.
+// diverging 1e8-fold, or — MTS mode — no new minimum in 200 iterations).  When the
+// recursion converges but the true residual fails the test, the run restarts from the
+// true residual (iterative refinement with the same preconditioner), at most 4 times.
+// `it` accumulates iterations across runs.
 __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int nLf, double wn,
-                       int& it, int cap, double& relres) {
+                       int& it, int cap, double& relres, double rel_tol, double inner_tol) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
   double* hS = F.S<double>(L.s_h);
   double* rS = F.S<double>(L.s_r);
-  const double tol = P.pcg_rel_tol * wn;
+  const double tol = rel_tol * wn;            // acceptance on the true residual
+  const double itol = fmin(inner_tol, rel_tol) * wn;   // recursion target
   double* zS = F.S<double>(L.s_z);
   double* fS = F.S<double>(L.s_f);
   for (int j = F.lane; j < C.m; j += 32) {
@@ -756,8 +785,11 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
     bool conv = false, bad = false;
     double rrmin = 1e308;
     int since_min = 0;
+    long long tk = clock64();
     while (it < cap) {
+      ALP_TICK(F, CY_PCG, tk);
       double hl = spmv<false>(F);   // line 6: l = Q h
+      ALP_TICK(F, CY_SPMV, tk);
       if (!(hl > 0.0) || !isfinite(hl)) {
         bad = true;
         break;
@@ -774,19 +806,27 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
       __syncwarp();
       rr = wsum(rr);
       ++it;
-      if (sqrt(rr) <= tol) {
+      if (sqrt(rr) <= itol) {
         conv = true;
         break;
       }
       if (rr < rrmin) {
         rrmin = rr;
         since_min = 0;
-      } else if (mode == PC_MTS && (rr > 1e16 * rrmin || ++since_min > 200)) {
-        bad = true;
-        break;
+      } else if (rr > 1e16 * rrmin || ++since_min > (mode == PC_MTS ? 200 : 1000)) {
+        if (rrmin <= tol * tol) {   // stalled below the acceptance tolerance: good enough
+          conv = true;
+          break;
+        }
+        if (mode == PC_MTS) {
+          bad = true;
+          break;
+        }
       }
       double rz_new;
+      ALP_TICK(F, CY_PCG, tk);
       precond_apply(F, mode, nLb, nLf, rz_new);   // line 10
+      ALP_TICK(F, CY_SWEEP, tk);
       if (!(rz_new > 0.0) || !isfinite(rz_new)) {
         bad = true;
         break;
@@ -799,6 +839,7 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
       }
       __syncwarp();
     }
+    ALP_TICK(F, CY_PCG, tk);
     if (bad) return ST_PCG_BREAKDOWN;
     // true residual r = w - Q dy (h <- dy; h is rebuilt on restart)
     for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
@@ -824,9 +865,25 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
     aa = sqrt(wsum(aa));
     if (trn <= 16.0 * 2.220446049250313e-16 * aa) return ST_PCG_FLOOR;
     if (!conv) return ST_PCG_MAXITER;
-    if (mode == PC_MTS) return ST_PCG_BREAKDOWN;   // recursion and truth disagree
+    // the recursion converged but the true residual did not: restart from it
   }
   return ST_PCG_MAXITER;
+}
+
+// 1/diag(Q), diag(Q)_j = sum_{i in N(j)} d2_i + d2_{n+j} (A entries are +-1), into dinvF
+// (the MTS sweep program's scale factors are dead once a solve falls back).
+__device__ void jacobi_setup(const Frame& F) {
+  const DCode& C = *F.C;
+  for (int j = F.lane; j < C.m; j += 32) {
+    double dq = 0.0;
+    if (F.sgnC[j] & PRESENT) {
+      dq = F.d2[C.n + j];
+      int deg = C.chk_deg[j];
+      for (int t = 0; t < deg; ++t) dq += F.d2[chk_nb(C, j, t)];
+    }
+    F.dinvF[j] = (dq > 0.0) ? 1.0 / dq : 0.0;
+  }
+  __syncwarp();
 }
 
 // Step solve of eq.`Delta y` by PCG.  precond = 0: the paper's column-wise MTS
@@ -834,10 +891,12 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
 // basic columns (Remark P:807-810); kappa(M^-1 Q) then explodes and the fp64 recursion
 // decouples from the true residual.  So (R-2): an MTS run that breaks down,
 // stalls, or whose TRUE residual is above tol (a floor-limited result above 1e-6 ||w||
-// included) is followed by a plain-CG run from dy = 0 (ST_PCG_FALLBACK,
-// informational), and the better of the two results is kept.  precond = 1: plain CG only.
+// included) is followed by a Jacobi-preconditioned CG run from dy = 0 to
+// pcg_fallback_tol (ST_PCG_FALLBACK, informational) within the iteration cap, and the
+// better of the two results is kept.  precond = 1: plain CG only.
 // w is read from F.w; the solution is left in F.dy.
-__device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, int nLb, int nLf) {
+__device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, int nLb, int nLf,
+                               double inner_tol) {
   const DCode& C = *F.C;
   double ww = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
@@ -851,12 +910,13 @@ __device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, in
   if (wn == 0.0) return res;
   int it = 0;
   if (!use_mtm) {
-    res.status = pcg_run(F, P, PC_NONE, 0, 0, wn, it, P.pcg_max_iter, res.relres);
+    res.status = pcg_run(F, P, PC_NONE, 0, 0, wn, it, P.pcg_max_iter, res.relres, P.pcg_rel_tol,
+                         inner_tol);
     res.iters = it;
     return res;
   }
   double rel1 = 1.0;
-  int st1 = pcg_run(F, P, PC_MTS, nLb, nLf, wn, it, P.pcg_max_iter, rel1);
+  int st1 = pcg_run(F, P, PC_MTS, nLb, nLf, wn, it, P.pcg_max_iter, rel1, P.pcg_rel_tol, inner_tol);
   if (st1 == 0 || (st1 == ST_PCG_FLOOR && rel1 <= 1e-6)) {
     res.status = st1;
     res.relres = rel1;
@@ -867,10 +927,13 @@ __device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, in
   if (keep1)
     for (int j = F.lane; j < C.m; j += 32) F.dyb[j] = F.dy[j];
   __syncwarp();
+  jacobi_setup(F);
   int it2 = 0;
   double rel2 = 1.0;
-  int st2 = pcg_run(F, P, PC_NONE, 0, 0, wn, it2, P.pcg_max_iter, rel2);
+  int st2 = pcg_run(F, P, PC_JACOBI, 0, 0, wn, it2, P.pcg_max_iter, rel2, P.pcg_fallback_tol,
+                    inner_tol);
   res.iters = it + it2;
+  if (st2 != 0 && st2 != ST_PCG_BREAKDOWN && rel2 <= P.pcg_rel_tol) st2 = 0;   // met the C-9 test
   if (keep1 && (st2 != 0) && !(st2 == ST_PCG_FLOOR && rel2 <= rel1)) {
     for (int j = F.lane; j < C.m; j += 32) F.dy[j] = F.dyb[j];
     __syncwarp();

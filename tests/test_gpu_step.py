@@ -94,10 +94,14 @@ def test_golden_step_system():
 
 
 def test_c5_shaped_systems_vs_oracle():
+    """Config 5 (kappa(Q) up to ~1e18): forward error vs the exact solve <= 1e-6 (reading
+    C-27: relres <= 1e-8 bounds the error only by kappa * 1e-8; fp64 Cholesky's own error
+    reaches 5e-7 on these systems)."""
     code = config_code(5)
     sy = c5_systems(range(24), code)
     out = _run(code, sy.masks, sy.d, sy.r)
-    errs = [_check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, s) for s in range(sy.S)]
+    errs = [_check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, s, tol_dy=1e-6)
+            for s in range(sy.S)]
     print("C5 rel err max %.2e, iters %s" % (max(errs), out["iters"].tolist()))
 
 
@@ -111,7 +115,7 @@ def test_partial_rows_flips_and_ragged_batches(S):
     for s in range(S):
         if (sy.masks[s] >> 15).sum() == 0:
             continue
-        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], flip[s], out, s)
+        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], flip[s], out, s, tol_dy=1e-7)
 
 
 def test_plain_cg_option():
@@ -120,7 +124,8 @@ def test_plain_cg_option():
     out = _run(code, sy.masks, sy.d, sy.r, precond=1)
     assert np.all(out["prow"] == -1)
     for s in range(8):
-        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, s, tol_dy=1e-8, check_pivots=False)
+        # kappa(Q) ~ 5 here: forward error <= kappa * relres ~ 5e-8
+        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, s, tol_dy=1e-7, check_pivots=False)
 
 
 def test_empty_batch_and_all_absent_rows():
@@ -150,4 +155,4 @@ def test_c5_full_size_properties_and_sampled_parity():
     print("C5 full: status counts", dict(zip(*[a.tolist() for a in np.unique(st, return_counts=True)])),
           "iters mean %.1f max %d" % (out["iters"].mean(), out["iters"].max()))
     for s in np.random.default_rng(0).choice(S, 16, replace=False):
-        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, int(s))
+        _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, int(s), tol_dy=1e-6)

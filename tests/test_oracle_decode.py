@@ -153,3 +153,22 @@ def test_codeword_enumeration_h1():
     code = code_from_rows([[0, 1, 2], [1, 2, 3]], 4, "H1")
     words = sorted("".join(map(str, w)) for w in codewords(code))
     assert words == ["0000", "0110", "1011", "1101"]
+
+
+def test_malp_cycle_detection_stops_at_a_repeated_pool():
+    """Reading C-12: MALP-A is a deterministic function of its cut pool, so a pool equal to
+    that of an LP already solved cycles forever.  On this C2 frame (3.0 dB) the oracle used
+    to run to the 200-LP cap; it must now stop at the first repeat with ALP_MAXITER, and the
+    pool it stopped on must equal the pool of one of the LPs it solved."""
+    from oracle.lp import mask_word, ST_ALP_MAXITER
+    from synth import config_code, config_frames
+    code = config_code(2)
+    fb = config_frames(2, 2, frames=[1737])
+    o = malp_decode(code, fb.llr[0], record=True)
+    assert o["status"] & ST_ALP_MAXITER
+    assert o["lp_solves"] < 20
+    final = {j: mask_word(v) for j, v in o["pool"].items()}
+    assert any(final == {j: mask_word(v) for j, v in tr["pool"].items()} for tr in o["trace"])
+    # the solved LPs themselves were all distinct
+    keys = [frozenset((j, mask_word(v)) for j, v in tr["pool"].items()) for tr in o["trace"]]
+    assert len(set(keys)) == len(keys)

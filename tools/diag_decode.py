@@ -145,10 +145,10 @@ def c5_report():
 GAP = float(os.environ.get("GAP", "1e-9"))
 
 
-def c2_sample(F=512, snr_idx=0):
+def c2_sample(F=512, snr_idx=0, cfg=2):
     import time
-    code = config_code(2)
-    fb = config_frames(2, snr_idx, frames=range(F))
+    code = config_code(cfg)
+    fb = config_frames(cfg, snr_idx, frames=range(F))
     c = alp.Code.from_synth(code)
     llr = torch.from_numpy(fb.llr).cuda()
     params = alp.default_params(gap_tol=GAP)
@@ -161,12 +161,22 @@ def c2_sample(F=512, snr_idx=0):
     st = res.stats_numpy()
     status = res.status.cpu().numpy()
     vals, cnts = np.unique(status, return_counts=True)
-    print(f"C2 snr{snr_idx} F={F}: {dt*1e3:.1f} ms ({F/dt:.0f} frames/s); status counts {dict(zip(vals.tolist(), cnts.tolist()))}")
+    print(f"C{cfg} snr{snr_idx} F={F}: {dt*1e3:.1f} ms ({F/dt:.0f} frames/s); status counts {dict(zip(vals.tolist(), cnts.tolist()))}")
     print("   lp/frame %.2f ipm/frame %.1f pcg/frame %.0f pcg/ipm %.1f max_p mean %.0f; cert %d/%d" % (
         st["lp_solves"].mean(), st["ipm_iters"].mean(), st["pcg_iters"].mean(),
         st["pcg_iters"].sum() / max(1, st["ipm_iters"].sum()), st["max_p"].mean(), int(res.certificate.sum()), F))
     hard = res.hard.cpu().numpy()
     print("   frame errors vs tx:", int(np.any(hard != fb.codewords, axis=1).sum()))
+    cyc = {k: float(st[k].sum()) for k in ("cyc_cut", "cyc_ipm", "cyc_build", "cyc_spmv", "cyc_sweep", "cyc_pcg_other")}
+    tot = sum(cyc.values())
+    print("   phase shares:", {k: round(v / tot, 3) for k, v in cyc.items()},
+          "cycles/PCG-iter %.0f (spmv %.0f sweep %.0f other %.0f)" % (
+              (cyc["cyc_spmv"] + cyc["cyc_sweep"] + cyc["cyc_pcg_other"]) / st["pcg_iters"].sum(),
+              cyc["cyc_spmv"] / st["pcg_iters"].sum(), cyc["cyc_sweep"] / st["pcg_iters"].sum(),
+              cyc["cyc_pcg_other"] / st["pcg_iters"].sum()),
+          "build cycles/IPM-iter %.0f" % (cyc["cyc_build"] / st["ipm_iters"].sum()))
+    lat = np.argsort(-st["pcg_iters"])[:5]
+    print("   slowest frames (pcg its):", [(int(f), int(st["pcg_iters"][f]), int(st["lp_solves"][f]), int(st["ipm_iters"][f]), int(status[f])) for f in lat])
     from oracle.lp import params_with
     obj = res.objective.cpu().numpy()
     worst = 0.0
@@ -183,3 +193,4 @@ if __name__ == "__main__":
         main()
     c2_sample()
     c2_sample(F=2048, snr_idx=2)
+    c2_sample(F=256, snr_idx=0, cfg=3)
