@@ -16,7 +16,7 @@ class AlpParams(C.Structure):
         ("pcg_fallback_tol", C.c_double),
         ("tau_viol", C.c_double), ("tau_act", C.c_double), ("tau_cert", C.c_double),
         ("alp_max_iter", C.c_int32), ("ipm_max_iter", C.c_int32), ("pcg_max_iter", C.c_int32),
-        ("warps_per_block", C.c_int32),
+        ("warps_per_block", C.c_int32), ("smem_frames_per_sm", C.c_int32),
     ]
 
 

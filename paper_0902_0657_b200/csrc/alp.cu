@@ -439,9 +439,9 @@ using namespace alp;
 
 struct alp_code {
   int n, m, dc, dv, E;
-  int* d_chk_var;
+  uint16_t* d_chk_var;
   uint8_t* d_chk_deg;
-  int* d_var_chk;
+  uint16_t* d_var_chk;
   uint8_t* d_var_slot;
   uint8_t* d_var_deg;
 };
@@ -482,7 +482,7 @@ DCode make_dcode(const alp_code* c) {
   return C;
 }
 
-Layout make_layout(const DCode& C) {
+Layout make_layout(const DCode& C, int smem_budget) {
   Layout L;
   const size_t n = C.n, m = C.m, Q = C.Q;
   size_t o = 0;
@@ -559,9 +559,32 @@ Layout make_layout(const DCode& C) {
     L.s_t = s(8 * n);
     end_pcg = a;
   }
-  size_t tot = std::max(s_sort, std::max(end_peel, end_pcg));
+  size_t tot = al(std::max(s_sort, std::max(end_peel, end_pcg)), 16);
+  // Relocate the arrays the PCG loop touches every iteration into the shared window, by
+  // priority (sweep program, sign tables, D^2, l, dy, w), while the window fits the budget.
+  L.smask = 0;
+  const size_t rel_bytes[RL_N] = {4 * m * (size_t)C.RB, 4 * m * (size_t)RF, 4 * (m + 2), 4 * (m + 2),
+                                  8 * m, 2 * m, n, 8 * Q, 8 * m, 8 * m, 8 * m};
+  for (int k = 0; k < RL_N; ++k) {
+    size_t need = al(rel_bytes[k], 16);
+    if ((long long)(tot + need) > (long long)smem_budget) continue;
+    L.smask |= 1u << k;
+    L.soff[k] = (int)tot;
+    tot += need;
+  }
   L.smem_bytes = (int)al(tot, 128);
   return L;
+}
+
+// Shared-memory budget per warp (frame): the device's per-block opt-in limit split over
+// `frames_per_sm` resident frames.
+int smem_budget_for(const alp_params* p) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
+    optin = 227 * 1024;
+  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 12;
+  return (optin / fps) & ~127;
 }
 
 Params make_params(const alp_params* p) {
@@ -594,8 +617,8 @@ alp_status check_params(const alp_params* p) {
     return fail(ALP_ERR_INVALID_ARG, "params.sigma and params.eta must lie in (0,1)");
   if (p->alp_max_iter < 0 || p->alp_max_iter > 255 || p->ipm_max_iter < 0 || p->pcg_max_iter < 1)
     return fail(ALP_ERR_INVALID_ARG, "iteration caps: 0 <= alp_max_iter <= 255, ipm >= 0, pcg >= 1");
-  if (p->warps_per_block < 0 || p->warps_per_block > 4)
-    return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..4");
+  if (p->warps_per_block < 0 || p->warps_per_block > 4 || p->smem_frames_per_sm < 0 || p->smem_frames_per_sm > 32)
+    return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..4, smem_frames_per_sm 0..32");
   return ALP_OK;
 }
 
@@ -658,6 +681,7 @@ void alp_default_params(alp_params* p) {
   p->ipm_max_iter = 100;
   p->pcg_max_iter = 1000;
   p->warps_per_block = 0;
+  p->smem_frames_per_sm = 0;
 }
 
 const char* alp_status_string(alp_status s) {
@@ -718,16 +742,16 @@ alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const i
   if (dv > DVMAX) return fail(ALP_ERR_UNSUPPORTED, "variable degree > 4");
   if ((long long)n + m > 65535) return fail(ALP_ERR_UNSUPPORTED, "n + m > 65535");
   if (dv == 0) dv = 1;
-  std::vector<int> chk_var((size_t)m * dc, -1), var_chk((size_t)n * dv, -1);
+  std::vector<uint16_t> chk_var((size_t)m * dc, 0xffff), var_chk((size_t)n * dv, 0xffff);
   std::vector<uint8_t> chk_deg(m), var_slot((size_t)n * dv, 0), var_deg(n, 0);
   for (int j = 0; j < m; ++j) {
     int a = row_ptr[j], b = row_ptr[j + 1];
     chk_deg[j] = (uint8_t)(b - a);
     for (int t = a; t < b; ++t) {
       int i = col_idx[t];
-      chk_var[(size_t)j * dc + (t - a)] = i;
+      chk_var[(size_t)j * dc + (t - a)] = (uint16_t)i;
       int k = var_deg[i]++;
-      var_chk[(size_t)i * dv + k] = j;
+      var_chk[(size_t)i * dv + k] = (uint16_t)j;
       var_slot[(size_t)i * dv + k] = (uint8_t)(t - a);
     }
   }
@@ -747,9 +771,9 @@ alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const i
   c->d_chk_var = nullptr;
   c->d_chk_deg = c->d_var_slot = c->d_var_deg = nullptr;
   c->d_var_chk = nullptr;
-  bool ok = up((void**)&c->d_chk_var, chk_var.data(), chk_var.size() * 4) &&
+  bool ok = up((void**)&c->d_chk_var, chk_var.data(), chk_var.size() * 2) &&
             up((void**)&c->d_chk_deg, chk_deg.data(), chk_deg.size()) &&
-            up((void**)&c->d_var_chk, var_chk.data(), var_chk.size() * 4) &&
+            up((void**)&c->d_var_chk, var_chk.data(), var_chk.size() * 2) &&
             up((void**)&c->d_var_slot, var_slot.data(), var_slot.size()) &&
             up((void**)&c->d_var_deg, var_deg.data(), var_deg.size());
   if (!ok) {
@@ -778,7 +802,7 @@ size_t alp_decode_workspace_bytes(const alp_code* code, int64_t n_frames, const 
     return 0;
   }
   DCode C = make_dcode(code);
-  Layout L = make_layout(C);
+  Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
   if (plan_launch(alp_decode_kernel, L, std::max<int64_t>(n_frames, 1), params, cfg) != ALP_OK) return 0;
   return kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
@@ -790,7 +814,7 @@ size_t alp_pcg_workspace_bytes(const alp_code* code, int64_t n_sys, const alp_pa
     return 0;
   }
   DCode C = make_dcode(code);
-  Layout L = make_layout(C);
+  Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
   if (plan_launch(pcg_step_kernel, L, std::max<int64_t>(n_sys, 1), params, cfg) != ALP_OK) return 0;
   return kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
@@ -812,7 +836,7 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
   if (!workspace || ((uintptr_t)workspace & 255))
     return fail(ALP_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
   DCode C = make_dcode(code);
-  Layout L = make_layout(C);
+  Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
   alp_status st = plan_launch(alp_decode_kernel, L, n_frames, params, cfg);
   if (st != ALP_OK) return st;
@@ -903,7 +927,7 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   if (!workspace || ((uintptr_t)workspace & 255))
     return fail(ALP_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
   DCode C = make_dcode(code);
-  Layout L = make_layout(C);
+  Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
   alp_status st = plan_launch(pcg_step_kernel, L, n_sys, params, cfg);
   if (st != ALP_OK) return st;

@@ -33,9 +33,9 @@ struct Params {
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
 struct DCode {
   int n, m, dc, dv, Q, QP2, W, RB;        // Q = n + m columns, QP2 = pow2 >= Q, W = bitmap words
-  const int* __restrict__ chk_var;        // [m][dc] sorted variables of each check, -1 padded
+  const uint16_t* __restrict__ chk_var;   // [m][dc] sorted variables of each check, 0xffff padded
   const uint8_t* __restrict__ chk_deg;    // [m]
-  const int* __restrict__ var_chk;        // [n][dv] checks of each variable, -1 padded
+  const uint16_t* __restrict__ var_chk;   // [n][dv] checks of each variable, 0xffff padded
   const uint8_t* __restrict__ var_slot;   // [n][dv] position t of the variable in N(check)
   const uint8_t* __restrict__ var_deg;    // [n]
 };
@@ -46,6 +46,10 @@ struct Layout {
   long long g_cyc, g_x, g_z, g_d2, g_v, g_y, g_dy, g_dyb, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
       g_offF, g_sgnC, g_mask, g_hist, g_prc, g_sgnV, g_flip;
   int smem_bytes;
+  // Hot per-frame arrays that live in the warp's shared window instead of the slot
+  // (bit k of smask set <=> array k at shared offset soff[k]); order = placement priority.
+  unsigned smask;
+  int soff[12];
   int s_keys;                                                                  // sort phase
   int s_order, s_rank, s_cnt, s_xr, s_bm, s_pos, s_pcol, s_prow, s_lvB, s_lvF;  // peel phase
   int s_poc, s_hist, s_cur;                                                    // post-peel
@@ -109,6 +113,13 @@ struct Frame {
   __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(sm + off); }
 };
 
+enum { RL_RECB = 0, RL_RECF, RL_OFFB, RL_OFFF, RL_DINVF, RL_SGNC, RL_SGNV, RL_D2, RL_L, RL_DY, RL_W,
+       RL_N };
+
+__device__ __forceinline__ char* rel_ptr(const Layout* L, char* slot, char* sm, int k, long long g) {
+  return ((L->smask >> k) & 1u) ? sm + L->soff[k] : slot + g;
+}
+
 __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layout* L, char* slot,
                                            char* sm, int lane) {
   F.C = C;
@@ -136,15 +147,28 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.mask = (uint16_t*)(slot + L->g_mask);
   F.prc = (uint16_t*)(slot + L->g_prc);
   F.hist = (unsigned long long*)(slot + L->g_hist);
+  F.recB = (int*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
+  F.recF = (int*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
+  F.offB = (int*)rel_ptr(L, slot, sm, RL_OFFB, L->g_offB);
+  F.offF = (int*)rel_ptr(L, slot, sm, RL_OFFF, L->g_offF);
+  F.dinvF = (double*)rel_ptr(L, slot, sm, RL_DINVF, L->g_dinvF);
+  F.sgnC = (uint16_t*)rel_ptr(L, slot, sm, RL_SGNC, L->g_sgnC);
+  F.sgnV = (uint8_t*)rel_ptr(L, slot, sm, RL_SGNV, L->g_sgnV);
+  F.d2 = (double*)rel_ptr(L, slot, sm, RL_D2, L->g_d2);
+  F.l = (double*)rel_ptr(L, slot, sm, RL_L, L->g_l);
+  F.dy = (double*)rel_ptr(L, slot, sm, RL_DY, L->g_dy);
+  F.w = (double*)rel_ptr(L, slot, sm, RL_W, L->g_w);
   F.sgnV = (uint8_t*)(slot + L->g_sgnV);
   F.flip = (uint8_t*)(slot + L->g_flip);
 }
 
 __device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
-  return __ldg(C.chk_var + j * C.dc + t);
+  const unsigned v = __ldg(C.chk_var + j * C.dc + t);
+  return v == 0xffffu ? -1 : (int)v;
 }
 __device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
-  return __ldg(C.var_chk + i * C.dv + k);
+  const unsigned v = __ldg(C.var_chk + i * C.dv + k);
+  return v == 0xffffu ? -1 : (int)v;
 }
 
 // =====================================================================================
@@ -627,30 +651,128 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 // Stops after line 9 once ||r||_2 <= tol ||w||_2 (G15).  h^T l <= 0 -> breakdown.
 // w is read from F.w; the solution accumulates in F.dy.
 // =====================================================================================
+// Sweep records are read as int4 vectors; each level's first 32-slot chunk is prefetched
+// during the previous level (offsets and records do not depend on the values being
+// computed), so a level costs one shared-memory gather round instead of three dependent
+// global loads.
+struct RecB {
+  int4 q[4];   // up to 16 ints: head + <= 15 deps (RB <= 16)
+};
+__device__ __forceinline__ void load_recB(const int* base, int RB, RecB& r) {
+  const int4* p = reinterpret_cast<const int4*>(base);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (4 * k < RB) r.q[k] = p[k];
+}
+__device__ __forceinline__ int rec_at(const RecB& r, int k) {   // k compile-time after unroll
+  const int* v = reinterpret_cast<const int*>(&r.q[0]);
+  return v[k];
+}
+
 // Back substitution A_M f = r over the level schedule (P:585 stage 1): r in s_r, f in s_f,
 // both indexed by pivot row; f_R is the component of row R's pivot column.
+__device__ __forceinline__ void back_step(const RecB& rec, const double* rS, double* fS) {
+  const int head = rec_at(rec, 0);
+  const int R = head & 0xffffff, nd = (head >> 24) & 0xf;
+  double acc = rS[R];
+#pragma unroll
+  for (int d = 0; d < DCMAX; ++d) {
+    if (d < nd) {
+      int dep = rec_at(rec, 1 + d);
+      double fv = fS[dep & 0x7fffffff];
+      acc = (dep < 0) ? acc + fv : acc - fv;
+    }
+  }
+  fS[R] = (head < 0) ? -acc : acc;
+}
+
 __device__ __forceinline__ void back_sweep(const Frame& F, int nLb) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
   const double* rS = F.S<double>(L.s_r);
   double* fS = F.S<double>(L.s_f);
   const int RB = C.RB;
+  if (nLb <= 0) return;
+  int a = F.offB[0], b = F.offB[1];
+  RecB cur;
+  bool hc = a + F.lane < b;
+  if (hc) load_recB(F.recB + (size_t)(a + F.lane) * RB, RB, cur);
   for (int lvl = 0; lvl < nLb; ++lvl) {
-    int s0 = F.offB[lvl], s1 = F.offB[lvl + 1];
-    for (int s = s0 + F.lane; s < s1; s += 32) {
-      const int* rec = F.recB + (size_t)s * RB;
-      int head = rec[0];
-      int R = head & 0xffffff, nd = (head >> 24) & 0xf;
-      double acc = rS[R];
-      for (int d = 0; d < nd; ++d) {
-        int dep = rec[1 + d];
-        double fv = fS[dep & 0x7fffffff];
-        acc = (dep < 0) ? acc + fv : acc - fv;
-      }
-      fS[R] = (head < 0) ? -acc : acc;
+    const int c = (lvl + 2 <= nLb) ? F.offB[lvl + 2] : b;
+    RecB nxt;
+    const bool hn = (lvl + 1 < nLb) && (b + F.lane < c);
+    if (hn) load_recB(F.recB + (size_t)(b + F.lane) * RB, RB, nxt);
+    if (hc) back_step(cur, rS, fS);
+    for (int s = a + F.lane + 32; s < b; s += 32) {
+      RecB t;
+      load_recB(F.recB + (size_t)s * RB, RB, t);
+      back_step(t, rS, fS);
     }
     __syncwarp();
+    a = b;
+    b = c;
+    cur = nxt;
+    hc = hn;
   }
+}
+
+// Forward substitution A_M^T z = D_M^-2 f (P:585 stages 2-3); returns this lane's part of
+// z^T r = f^T D_M^-2 f (a sum of squares).
+__device__ __forceinline__ double fwd_step(int4 rec, double dinv, const double* fS, double* zS) {
+  const int head = rec.x;
+  const int R = head & 0xffffff, nd = (head >> 24) & 0xf;
+  const double fr = fS[R];
+  double acc = fr * dinv;
+  if (nd > 0) {
+    double zv = zS[rec.y & 0x7fffffff];
+    acc = (rec.y < 0) ? acc + zv : acc - zv;
+  }
+  if (nd > 1) {
+    double zv = zS[rec.z & 0x7fffffff];
+    acc = (rec.z < 0) ? acc + zv : acc - zv;
+  }
+  if (nd > 2) {
+    double zv = zS[rec.w & 0x7fffffff];
+    acc = (rec.w < 0) ? acc + zv : acc - zv;
+  }
+  zS[R] = (head < 0) ? -acc : acc;
+  return fr * fr * dinv;
+}
+
+__device__ __forceinline__ double fwd_sweep(const Frame& F, int nLf) {
+  const Layout& L = *F.L;
+  const double* fS = F.S<double>(L.s_f);
+  double* zS = F.S<double>(L.s_z);
+  const int4* recF = reinterpret_cast<const int4*>(F.recF);   // RF == 4
+  double rz = 0.0;
+  if (nLf <= 0) return rz;
+  int a = F.offF[0], b = F.offF[1];
+  int4 cur = make_int4(0, 0, 0, 0);
+  double dcur = 0.0;
+  bool hc = a + F.lane < b;
+  if (hc) {
+    cur = recF[a + F.lane];
+    dcur = F.dinvF[a + F.lane];
+  }
+  for (int lvl = 0; lvl < nLf; ++lvl) {
+    const int c = (lvl + 2 <= nLf) ? F.offF[lvl + 2] : b;
+    int4 nxt = make_int4(0, 0, 0, 0);
+    double dnxt = 0.0;
+    const bool hn = (lvl + 1 < nLf) && (b + F.lane < c);
+    if (hn) {
+      nxt = recF[b + F.lane];
+      dnxt = F.dinvF[b + F.lane];
+    }
+    if (hc) rz += fwd_step(cur, dcur, fS, zS);
+    for (int s = a + F.lane + 32; s < b; s += 32) rz += fwd_step(recF[s], F.dinvF[s], fS, zS);
+    __syncwarp();
+    a = b;
+    b = c;
+    cur = nxt;
+    dcur = dnxt;
+    hc = hn;
+  }
+  return rz;
 }
 
 // Preconditioner modes of one PCG attempt.
@@ -676,25 +798,7 @@ __device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb,
     return;
   }
   back_sweep(F, nLb);
-  for (int lvl = 0; lvl < nLf; ++lvl) {
-    int s0 = F.offF[lvl], s1 = F.offF[lvl + 1];
-    for (int s = s0 + F.lane; s < s1; s += 32) {
-      const int* rec = F.recF + (size_t)s * RF;
-      int head = rec[0];
-      int R = head & 0xffffff, nd = (head >> 24) & 0xf;
-      double acc = fS[R] * F.dinvF[s];
-      for (int d = 0; d < nd; ++d) {
-        int dep = rec[1 + d];
-        double zv = zS[dep & 0x7fffffff];
-        acc = (dep < 0) ? acc + zv : acc - zv;
-      }
-      double zz = (head < 0) ? -acc : acc;
-      zS[R] = zz;
-      // z^T r = f^T D_M^-2 f (f = A_M^-1 r): a sum of squares, never <= 0 by cancellation
-      acc_rz += fS[R] * fS[R] * F.dinvF[s];
-    }
-    __syncwarp();
-  }
+  acc_rz = fwd_sweep(F, nLf);
   rz = wsum(acc_rz);
 }
 
@@ -713,33 +817,49 @@ __device__ __forceinline__ double spmv(const Frame& F) {
   const Layout& L = *F.L;
   const double* hS = F.S<double>(L.s_h);
   double* tS = F.S<double>(L.s_t);
+  const int dvs = C.dv, dcs = C.dc;
   double hl = 0.0;
+  // variable pass: t_i = d2_i (A^T h)_i; neighbour indices of all DVMAX slots are loaded
+  // first (predicated, independent) so the gathers of one variable overlap
   for (int i = F.lane; i < C.n; i += 32) {
-    uint8_t s = F.sgnV[i];
+    const uint8_t s = F.sgnV[i];
     if (!(s & 0xf)) continue;
-    int dv = C.var_deg[i];
+    const double d2i = F.d2[i];
+    int jn[DVMAX];
+#pragma unroll
+    for (int k = 0; k < DVMAX; ++k) jn[k] = (k < dvs && ((s >> k) & 1)) ? var_ck(C, i, k) : -1;
     double acc = 0.0;
-    for (int k = 0; k < dv; ++k) {
-      double hv = hS[var_ck(C, i, k)];
-      if (ABS) acc += fabs(hv);
-      else acc = ((s >> (4 + k)) & 1) ? acc - hv : acc + hv;
+#pragma unroll
+    for (int k = 0; k < DVMAX; ++k) {
+      if (jn[k] >= 0) {
+        double hv = hS[jn[k]];
+        if (ABS) acc += fabs(hv);
+        else acc = ((s >> (4 + k)) & 1) ? acc - hv : acc + hv;
+      }
     }
-    double tv = F.d2[i] * acc;
+    double tv = d2i * acc;
     tS[i] = tv;
     hl += acc * tv;
   }
   __syncwarp();
+  // check pass: l_j = sum_i A_ji t_i + d2_{n+j} h_j
   for (int j = F.lane; j < C.m; j += 32) {
-    uint16_t s = F.sgnC[j];
+    const uint16_t s = F.sgnC[j];
     if (!(s & PRESENT)) continue;
-    int deg = C.chk_deg[j];
-    double hj = hS[j];
-    double ds = F.d2[C.n + j] * (ABS ? fabs(hj) : hj);
+    const int deg = C.chk_deg[j];
+    const double hj = hS[j];
+    const double ds = F.d2[C.n + j] * (ABS ? fabs(hj) : hj);
+    int in[DCMAX];
+#pragma unroll
+    for (int t = 0; t < DCMAX; ++t) in[t] = (t < dcs && t < deg) ? chk_nb(C, j, t) : -1;
     double acc = ds;
-    for (int t = 0; t < deg; ++t) {
-      double tv = tS[chk_nb(C, j, t)];
-      if (ABS) acc += tv;
-      else acc = ((s >> t) & 1) ? acc - tv : acc + tv;
+#pragma unroll
+    for (int t = 0; t < DCMAX; ++t) {
+      if (in[t] >= 0) {
+        double tv = tS[in[t]];
+        if (ABS) acc += tv;
+        else acc = ((s >> t) & 1) ? acc - tv : acc + tv;
+      }
     }
     F.l[j] = acc;
     hl += hj * ds;
