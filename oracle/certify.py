@@ -8,7 +8,8 @@ LP solve.  Inputs are a decoder's final u, the duals y of its final pool LP (per
         lhs < 1 - tol_cut on any check, and -tol <= u <= 1 + tol;
   (ii)  (y, z = c - A^T y) is dual feasible for the final pool LP in augmented form
         (dual LP P:418-428 read as "maximize b^T y", G4): z_std >= -tol_z (1 + ||c||),
-        and the slack columns give z_{n+j} = -y_j >= -tol_z, i.e. y <= tol_z;
+        and the slack columns give z_{n+j} = -y_j >= -tol_z (1 + ||c||), i.e. y <= tol_z (1 + ||c||)
+        (the same relative scale as the IPM's dual-feasibility stop, reading C-8);
   (iii) weak duality: for every x feasible for the full LP (which satisfies the pool rows
         and 0 <= x_aug <= ub, ub = 1 on standard and d_j on slack columns)
         c^T x = b^T y + z^T x_aug >= LB := b^T y + sum_i min(0, z_i) ub_i,
@@ -62,7 +63,7 @@ def dual_certificate(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1e-7, t
         b = inV.sum() - 1.0 - np.sum(a[flip[Nj]])
         z[Nj] -= coef * y[j]
         LB += b * y[j]
-        if y[j] > tol_z:
+        if y[j] > tol_z * (1.0 + cn):
             out["ok"] = False
             out["reasons"].append(f"y[{j}] = {y[j]} > 0")
         slack_terms += min(0.0, -y[j]) * d
@@ -123,7 +124,7 @@ def dual_certificate_batch(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1
     flat = (np.arange(Fn)[:, None, None] * n + Nb[None, :, :])
     np.subtract.at(z.reshape(-1), flat[:, valid].reshape(-1), contrib[:, valid].reshape(-1))
     b = inV.sum(axis=2) - 1.0 - np.where(valid & fl, a, 0.0).sum(axis=2)
-    ok &= np.all(~present | (y <= tol_z), axis=1)
+    ok &= np.all(~present | (y <= tol_z * (1.0 + cn)[:, None]), axis=1)
     ok &= z.min(axis=1) >= -tol_z * (1.0 + cn)
     x = np.where(flip, 1.0 - u, u)
     UB = (c * x).sum(axis=1)

@@ -45,13 +45,26 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
   const DCode& C = *F.C;
   const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
   const double q = (double)(n + p);
+  // restrict-qualified views: the arrays never alias, which lets the unrolled loops below
+  // issue the next lane-iterations' loads before this one's stores
+  double* __restrict__ X = F.x;
+  double* __restrict__ Z = F.z;
+  double* __restrict__ Y = F.y;
+  double* __restrict__ V = F.v;
+  const double* __restrict__ B = F.b;
+  // (d2, w and dy are shared with build_precond / pcg_solve: plain pointers)
+  double* D2 = F.d2;
+  double* W = F.w;
+  const double* DY = F.dy;
+  const uint16_t* __restrict__ SC = F.sgnC;
+  const uint8_t* __restrict__ SV = F.sgnV;
   const double s0 = fmax(1.0, fmax(bmax, cmax));
   for (int c = lane; c < Q; c += 32) {
-    bool valid = (c < n) || (F.sgnC[c - n] & PRESENT);
-    F.x[c] = valid ? s0 : 0.0;
-    F.z[c] = valid ? s0 : 0.0;
+    bool valid = (c < n) || (SC[c - n] & PRESENT);
+    X[c] = valid ? s0 : 0.0;
+    Z[c] = valid ? s0 : 0.0;
   }
-  for (int j = lane; j < m; j += 32) F.y[j] = 0.0;
+  for (int j = lane; j < m; j += 32) Y[j] = 0.0;
   __syncwarp();
   IpmOut out{0, 0, 0, 0.0};
   long long tk = clock64();
@@ -60,36 +73,38 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
   int it = 0;
   while (true) {
     double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
+#pragma unroll 2
     for (int j = lane; j < m; j += 32) {
-      uint16_t s = F.sgnC[j];
+      uint16_t s = SC[j];
       if (!(s & PRESENT)) continue;
       int deg = C.chk_deg[j];
-      double acc = F.b[j] - F.x[n + j];
+      double acc = B[j] - X[n + j];
       for (int t = 0; t < deg; ++t) {
-        double xi = F.x[chk_nb(C, j, t)];
+        double xi = X[chk_nb(C, j, t)];
         acc = ((s >> t) & 1) ? acc + xi : acc - xi;
       }
-      F.w[j] = acc;
+      W[j] = acc;
       rbn = fmax(rbn, fabs(acc));
-      double rc = -F.y[j] - F.z[n + j];
-      F.v[n + j] = rc;
+      double rc = -Y[j] - Z[n + j];
+      V[n + j] = rc;
       rcn = fmax(rcn, fabs(rc));
-      gap += F.x[n + j] * F.z[n + j];
+      gap += X[n + j] * Z[n + j];
     }
+#pragma unroll 4
     for (int i = lane; i < n; i += 32) {
       double ci = fabs(g[i]);
-      uint8_t s = F.sgnV[i];
+      uint8_t s = SV[i];
       int dv = C.var_deg[i];
-      double acc = ci - F.z[i];
+      double acc = ci - Z[i];
       for (int k = 0; k < dv; ++k) {
         if (!((s >> k) & 1)) continue;
-        double yj = F.y[var_ck(C, i, k)];
+        double yj = Y[var_ck(C, i, k)];
         acc = ((s >> (4 + k)) & 1) ? acc + yj : acc - yj;
       }
-      F.v[i] = acc;
+      V[i] = acc;
       rcn = fmax(rcn, fabs(acc));
-      double xi = F.x[i];
-      gap += xi * F.z[i];
+      double xi = X[i];
+      gap += xi * Z[i];
       cx += ci * xi;
     }
     __syncwarp();
@@ -105,25 +120,27 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
       break;
     }
     const double mu = P.sigma * gap / q;
+#pragma unroll 4
     for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(F.sgnC[c - n] & PRESENT)) continue;
-      double xc = F.x[c], zc = F.z[c];
+      if (c >= n && !(SC[c - n] & PRESENT)) continue;
+      double xc = X[c], zc = Z[c];
       double d2 = xc / zc;
       double re = mu - xc * zc;
-      F.d2[c] = d2;
-      F.v[c] = d2 * F.v[c] - re / zc;
+      D2[c] = d2;
+      V[c] = d2 * V[c] - re / zc;
     }
     __syncwarp();
+#pragma unroll 2
     for (int j = lane; j < m; j += 32) {
-      uint16_t s = F.sgnC[j];
+      uint16_t s = SC[j];
       if (!(s & PRESENT)) continue;
       int deg = C.chk_deg[j];
-      double acc = F.w[j] + F.v[n + j];
+      double acc = W[j] + V[n + j];
       for (int t = 0; t < deg; ++t) {
-        double vi = F.v[chk_nb(C, j, t)];
+        double vi = V[chk_nb(C, j, t)];
         acc = ((s >> t) & 1) ? acc - vi : acc + vi;
       }
-      F.w[j] = acc;
+      W[j] = acc;
     }
     __syncwarp();
     int nLb = 0, nLf = 0;
@@ -142,9 +159,9 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
     if (g_trace) {
       double dmn = 1e308, dmx = 0.0;
       for (int c = lane; c < Q; c += 32) {
-        if (c >= n && !(F.sgnC[c - n] & PRESENT)) continue;
-        dmn = fmin(dmn, F.d2[c]);
-        dmx = fmax(dmx, F.d2[c]);
+        if (c >= n && !(SC[c - n] & PRESENT)) continue;
+        dmn = fmin(dmn, D2[c]);
+        dmx = fmax(dmx, D2[c]);
       }
       dmn = wmin(dmn);
       dmx = wmax(dmx);
@@ -157,35 +174,36 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
     out.pcg_iters += pr.iters;
     out.pcg_bytes += (double)pr.iters * Bmin;
     double ax = 1e308, az = 1e308;
+#pragma unroll 4
     for (int i = lane; i < n; i += 32) {
-      uint8_t s = F.sgnV[i];
+      uint8_t s = SV[i];
       int dv = C.var_deg[i];
       double atdy = 0.0;
       for (int k = 0; k < dv; ++k) {
         if (!((s >> k) & 1)) continue;
-        double d = F.dy[var_ck(C, i, k)];
+        double d = DY[var_ck(C, i, k)];
         atdy = ((s >> (4 + k)) & 1) ? atdy - d : atdy + d;
       }
-      double xc = F.x[i], zc = F.z[i];
-      double dx = F.d2[i] * atdy - F.v[i];
+      double xc = X[i], zc = Z[i];
+      double dx = D2[i] * atdy - V[i];
       double re = mu - xc * zc;
       double dz = (re - zc * dx) / xc;
       if (dx < 0.0) ax = fmin(ax, -xc / dx);
       if (dz < 0.0) az = fmin(az, -zc / dz);
-      F.v[i] = dx;
-      F.d2[i] = dz;
+      V[i] = dx;
+      D2[i] = dz;
     }
     for (int j = lane; j < m; j += 32) {
-      if (!(F.sgnC[j] & PRESENT)) continue;
+      if (!(SC[j] & PRESENT)) continue;
       int c = n + j;
-      double xc = F.x[c], zc = F.z[c];
-      double dx = F.d2[c] * F.dy[j] - F.v[c];
+      double xc = X[c], zc = Z[c];
+      double dx = D2[c] * DY[j] - V[c];
       double re = mu - xc * zc;
       double dz = (re - zc * dx) / xc;
       if (dx < 0.0) ax = fmin(ax, -xc / dx);
       if (dz < 0.0) az = fmin(az, -zc / dz);
-      F.v[c] = dx;
-      F.d2[c] = dz;
+      V[c] = dx;
+      D2[c] = dz;
     }
     __syncwarp();
     ax = wmin(ax);
@@ -193,18 +211,19 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
     const double bP = fmin(1.0, P.eta * ax);
     const double bD = fmin(1.0, P.eta * az);
     bool bad = false;
+#pragma unroll 4
     for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(F.sgnC[c - n] & PRESENT)) continue;
-      double xn = F.x[c] + bP * F.v[c];
-      double zn = F.z[c] + bD * F.d2[c];
-      F.x[c] = xn;
-      F.z[c] = zn;
+      if (c >= n && !(SC[c - n] & PRESENT)) continue;
+      double xn = X[c] + bP * V[c];
+      double zn = Z[c] + bD * D2[c];
+      X[c] = xn;
+      Z[c] = zn;
       bad |= !isfinite(xn) || !isfinite(zn);
     }
     for (int j = lane; j < m; j += 32) {
-      if (!(F.sgnC[j] & PRESENT)) continue;
-      double yn = F.y[j] + bD * F.dy[j];
-      F.y[j] = yn;
+      if (!(SC[j] & PRESENT)) continue;
+      double yn = Y[j] + bD * DY[j];
+      Y[j] = yn;
       bad |= !isfinite(yn);
     }
     __syncwarp();
@@ -561,10 +580,20 @@ Layout make_layout(const DCode& C, int smem_budget) {
   }
   size_t tot = al(std::max(s_sort, std::max(end_peel, end_pcg)), 16);
   // Relocate the arrays the PCG loop touches every iteration into the shared window, by
-  // priority (sweep program, sign tables, D^2, l, dy, w), while the window fits the budget.
+  // priority (sign tables, l, dy, sweep program, D^2, w), while the window fits the budget.
   L.smask = 0;
-  const size_t rel_bytes[RL_N] = {4 * m * (size_t)C.RB, 4 * m * (size_t)RF, 4 * (m + 2), 4 * (m + 2),
-                                  8 * m, 2 * m, n, 8 * Q, 8 * m, 8 * m, 8 * m};
+  size_t rel_bytes[RL_N];
+  rel_bytes[RL_SGNC] = 2 * m;
+  rel_bytes[RL_SGNV] = n;
+  rel_bytes[RL_L] = 8 * m;
+  rel_bytes[RL_DY] = 8 * m;
+  rel_bytes[RL_DINVF] = 8 * m;
+  rel_bytes[RL_OFFB] = 4 * (m + 2);
+  rel_bytes[RL_OFFF] = 4 * (m + 2);
+  rel_bytes[RL_RECF] = 4 * m * (size_t)RF;
+  rel_bytes[RL_RECB] = 4 * m * (size_t)C.RB;
+  rel_bytes[RL_D2] = 8 * Q;
+  rel_bytes[RL_W] = 8 * m;
   for (int k = 0; k < RL_N; ++k) {
     size_t need = al(rel_bytes[k], 16);
     if ((long long)(tot + need) > (long long)smem_budget) continue;
@@ -583,7 +612,7 @@ int smem_budget_for(const alp_params* p) {
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
     optin = 227 * 1024;
-  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 12;
+  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 8;
   return (optin / fps) & ~127;
 }
 

@@ -113,7 +113,7 @@ struct Frame {
   __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(sm + off); }
 };
 
-enum { RL_RECB = 0, RL_RECF, RL_OFFB, RL_OFFF, RL_DINVF, RL_SGNC, RL_SGNV, RL_D2, RL_L, RL_DY, RL_W,
+enum { RL_SGNC = 0, RL_SGNV, RL_L, RL_DY, RL_DINVF, RL_OFFB, RL_OFFF, RL_RECF, RL_RECB, RL_D2, RL_W,
        RL_N };
 
 __device__ __forceinline__ char* rel_ptr(const Layout* L, char* slot, char* sm, int k, long long g) {
@@ -655,6 +655,24 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 // during the previous level (offsets and records do not depend on the values being
 // computed), so a level costs one shared-memory gather round instead of three dependent
 // global loads.
+// Level offsets off[0..nL] held in registers: lane l keeps off[l] and off[32 + l]; levels
+// beyond 63 fall back to memory.  Loaded once per sweep (one round trip instead of one per
+// level).
+struct OffReg {
+  int a, b;
+  const int* mem;
+  __device__ __forceinline__ void load(const int* off, int nL, int lane) {
+    mem = off;
+    a = (lane <= nL) ? off[lane] : 0;
+    b = (32 + lane <= nL) ? off[32 + lane] : 0;
+  }
+  __device__ __forceinline__ int operator()(int l) const {   // l warp-uniform
+    if (l < 32) return __shfl_sync(FULL, a, l);
+    if (l < 64) return __shfl_sync(FULL, b, l - 32);
+    return mem[l];
+  }
+};
+
 struct RecB {
   int4 q[4];   // up to 16 ints: head + <= 15 deps (RB <= 16)
 };
@@ -693,12 +711,14 @@ __device__ __forceinline__ void back_sweep(const Frame& F, int nLb) {
   double* fS = F.S<double>(L.s_f);
   const int RB = C.RB;
   if (nLb <= 0) return;
-  int a = F.offB[0], b = F.offB[1];
+  OffReg off;
+  off.load(F.offB, nLb, F.lane);
+  int a = off(0), b = off(1);
   RecB cur;
   bool hc = a + F.lane < b;
   if (hc) load_recB(F.recB + (size_t)(a + F.lane) * RB, RB, cur);
   for (int lvl = 0; lvl < nLb; ++lvl) {
-    const int c = (lvl + 2 <= nLb) ? F.offB[lvl + 2] : b;
+    const int c = (lvl + 2 <= nLb) ? off(lvl + 2) : b;
     RecB nxt;
     const bool hn = (lvl + 1 < nLb) && (b + F.lane < c);
     if (hn) load_recB(F.recB + (size_t)(b + F.lane) * RB, RB, nxt);
@@ -746,7 +766,9 @@ __device__ __forceinline__ double fwd_sweep(const Frame& F, int nLf) {
   const int4* recF = reinterpret_cast<const int4*>(F.recF);   // RF == 4
   double rz = 0.0;
   if (nLf <= 0) return rz;
-  int a = F.offF[0], b = F.offF[1];
+  OffReg off;
+  off.load(F.offF, nLf, F.lane);
+  int a = off(0), b = off(1);
   int4 cur = make_int4(0, 0, 0, 0);
   double dcur = 0.0;
   bool hc = a + F.lane < b;
@@ -755,7 +777,7 @@ __device__ __forceinline__ double fwd_sweep(const Frame& F, int nLf) {
     dcur = F.dinvF[a + F.lane];
   }
   for (int lvl = 0; lvl < nLf; ++lvl) {
-    const int c = (lvl + 2 <= nLf) ? F.offF[lvl + 2] : b;
+    const int c = (lvl + 2 <= nLf) ? off(lvl + 2) : b;
     int4 nxt = make_int4(0, 0, 0, 0);
     double dnxt = 0.0;
     const bool hn = (lvl + 1 < nLf) && (b + F.lane < c);
@@ -817,52 +839,86 @@ __device__ __forceinline__ double spmv(const Frame& F) {
   const Layout& L = *F.L;
   const double* hS = F.S<double>(L.s_h);
   double* tS = F.S<double>(L.s_t);
-  const int dvs = C.dv, dcs = C.dc;
+  const int dcs = C.dc;
   double hl = 0.0;
-  // variable pass: t_i = d2_i (A^T h)_i; neighbour indices of all DVMAX slots are loaded
-  // first (predicated, independent) so the gathers of one variable overlap
-  for (int i = F.lane; i < C.n; i += 32) {
-    const uint8_t s = F.sgnV[i];
-    if (!(s & 0xf)) continue;
-    const double d2i = F.d2[i];
-    int jn[DVMAX];
+  // variable pass, U variables per lane per step: all their index / sign / weight loads are
+  // issued before any gather, and all gathers before any store (the shared-memory store of
+  // t would otherwise block hoisting the next variable's loads)
+  constexpr int U = 2;
+  for (int i0 = F.lane; i0 < C.n; i0 += 32 * U) {
+    uint8_t sv[U];
+    double dv[U];
+    int jn[U][DVMAX];
 #pragma unroll
-    for (int k = 0; k < DVMAX; ++k) jn[k] = (k < dvs && ((s >> k) & 1)) ? var_ck(C, i, k) : -1;
-    double acc = 0.0;
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + 32 * u;
+      const bool ok = i < C.n;
+      sv[u] = ok ? F.sgnV[i] : (uint8_t)0;
+      dv[u] = ok ? F.d2[i] : 0.0;
 #pragma unroll
-    for (int k = 0; k < DVMAX; ++k) {
-      if (jn[k] >= 0) {
-        double hv = hS[jn[k]];
-        if (ABS) acc += fabs(hv);
-        else acc = ((s >> (4 + k)) & 1) ? acc - hv : acc + hv;
+      for (int k = 0; k < DVMAX; ++k)
+        jn[u][k] = (ok && k < C.dv && ((sv[u] >> k) & 1)) ? var_ck(C, i, k) : -1;
+    }
+    double acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc[u] = 0.0;
+#pragma unroll
+      for (int k = 0; k < DVMAX; ++k) {
+        if (jn[u][k] >= 0) {
+          double hv = hS[jn[u][k]];
+          if (ABS) acc[u] += fabs(hv);
+          else acc[u] = ((sv[u] >> (4 + k)) & 1) ? acc[u] - hv : acc[u] + hv;
+        }
       }
     }
-    double tv = d2i * acc;
-    tS[i] = tv;
-    hl += acc * tv;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + 32 * u;
+      if (i < C.n && (sv[u] & 0xf)) {
+        const double tv = dv[u] * acc[u];
+        tS[i] = tv;
+        hl += acc[u] * tv;
+      }
+    }
   }
   __syncwarp();
-  // check pass: l_j = sum_i A_ji t_i + d2_{n+j} h_j
-  for (int j = F.lane; j < C.m; j += 32) {
-    const uint16_t s = F.sgnC[j];
-    if (!(s & PRESENT)) continue;
-    const int deg = C.chk_deg[j];
-    const double hj = hS[j];
-    const double ds = F.d2[C.n + j] * (ABS ? fabs(hj) : hj);
-    int in[DCMAX];
+  // check pass: l_j = sum_i A_ji t_i + d2_{n+j} h_j, two checks per lane per step
+  for (int j0 = F.lane; j0 < C.m; j0 += 64) {
+    uint16_t sc[2];
+    double hj[2], d2s[2];
+    int in[2][DCMAX];
 #pragma unroll
-    for (int t = 0; t < DCMAX; ++t) in[t] = (t < dcs && t < deg) ? chk_nb(C, j, t) : -1;
-    double acc = ds;
+    for (int u = 0; u < 2; ++u) {
+      const int j = j0 + 32 * u;
+      const bool ok = j < C.m;
+      sc[u] = ok ? F.sgnC[j] : (uint16_t)0;
+      const int deg = ok ? (int)C.chk_deg[j] : 0;
+      hj[u] = ok ? hS[j] : 0.0;
+      d2s[u] = ok ? F.d2[C.n + j] : 0.0;
 #pragma unroll
-    for (int t = 0; t < DCMAX; ++t) {
-      if (in[t] >= 0) {
-        double tv = tS[in[t]];
-        if (ABS) acc += tv;
-        else acc = ((s >> t) & 1) ? acc - tv : acc + tv;
-      }
+      for (int t = 0; t < DCMAX; ++t) in[u][t] = (t < dcs && t < deg) ? chk_nb(C, j, t) : -1;
     }
-    F.l[j] = acc;
-    hl += hj * ds;
+    double acc[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double ds = d2s[u] * (ABS ? fabs(hj[u]) : hj[u]);
+      acc[u] = ds;
+#pragma unroll
+      for (int t = 0; t < DCMAX; ++t) {
+        if (in[u][t] >= 0) {
+          double tv = tS[in[u][t]];
+          if (ABS) acc[u] += tv;
+          else acc[u] = ((sc[u] >> t) & 1) ? acc[u] - tv : acc[u] + tv;
+        }
+      }
+      if (sc[u] & PRESENT) hl += hj[u] * ds;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = j0 + 32 * u;
+      if (j < C.m && (sc[u] & PRESENT)) F.l[j] = acc[u];
+    }
   }
   __syncwarp();
   return ABS ? 0.0 : wsum(hl);
@@ -916,12 +972,18 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
       }
       const double alpha = rz / hl;   // line 7
       double rr = 0.0;
-      for (int j = F.lane; j < C.m; j += 32) {
-        if (!(F.sgnC[j] & PRESENT)) continue;
-        F.dy[j] += alpha * hS[j];   // line 8
-        double r = rS[j] - alpha * F.l[j];   // line 9
-        rS[j] = r;
-        rr += r * r;
+      {
+        double* __restrict__ dyp = F.dy;
+        const double* __restrict__ lp = F.l;
+        const uint16_t* __restrict__ sc = F.sgnC;
+#pragma unroll 4
+        for (int j = F.lane; j < C.m; j += 32) {
+          if (!(sc[j] & PRESENT)) continue;
+          dyp[j] += alpha * hS[j];   // line 8
+          double r = rS[j] - alpha * lp[j];   // line 9
+          rS[j] = r;
+          rr += r * r;
+        }
       }
       __syncwarp();
       rr = wsum(rr);
@@ -953,6 +1015,7 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
       }
       const double nu = rz_new / rz;   // line 11
       rz = rz_new;
+#pragma unroll 4
       for (int j = F.lane; j < C.m; j += 32) {
         if (!(F.sgnC[j] & PRESENT)) continue;
         hS[j] = zS[j] + nu * hS[j];   // line 12

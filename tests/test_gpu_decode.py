@@ -81,6 +81,11 @@ def assert_certified(code, llr, g, min_clean=1.0):
     cert = dual_certificate_batch(code, llr[sel], g["u"][sel], g["y"][sel], g["masks"][sel])
     badm = ~cert["ok"]
     bad = sel[badm]
+    if bad.size:
+        from oracle.certify import dual_certificate
+        f = int(bad[0])
+        why = dual_certificate(code, llr[f], g["u"][f], g["y"][f], g["masks"][f])
+        print("P6 failure detail, frame", f, why.get("reasons"))
     assert bad.size == 0, (f"P6 certificate fails on frames {bad[:10]}: min_lhs "
                            f"{cert['min_lhs'][badm][:5]}, gap {cert['gap'][badm][:5]}, "
                            f"UB {cert['UB'][badm][:5]}, status {g['status'][bad[:5]]}")
