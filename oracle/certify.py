@@ -23,7 +23,7 @@ import numpy as np
 from .lp import find_violated_cut
 
 
-def dual_certificate(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1e-7, tol_z=1e-7,
+def dual_certificate(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1.001e-6, tol_z=1e-7,
                      tol_gap=1e-6):
     gamma = np.asarray(gamma, dtype=np.float64)
     u = np.asarray(u, dtype=np.float64)
@@ -81,7 +81,7 @@ def dual_certificate(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1e-7, t
     return out
 
 
-def dual_certificate_batch(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1e-7, tol_z=1e-7,
+def dual_certificate_batch(code, gamma, u, y, masks, tol_cut=1.001e-6, tol_box=1.001e-6, tol_z=1e-7,
                            tol_gap=1e-6):
     """dual_certificate over a batch of frames ([F, n] / [F, m] arrays), vectorised with numpy
     (same three checks, same tolerances).  Returns a dict of per-frame arrays incl. ok."""
