@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
+    ap.add_argument("--step-systems", type=int, default=65536,
+                    help="config-5 isolated step solves timed beside the decode (0 = skip)")
     return ap.parse_args()
 
 
@@ -339,6 +341,8 @@ def run_ours(args):
     if not args.no_e2e:
         line["e2e"] = {"value": total_frames / e2e_max, "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if args.step_systems > 0:
+        line["step_solve"] = time_step_solve(args, dev, stream)
     if ws == 1 and not args.no_cpu_baseline:
         fps, cores, nf, wall = time_oracle(args.snr_idx, args.cpu_seconds)
         line["cpu_baseline"] = {
@@ -349,6 +353,47 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def time_step_solve(args, dev, stream):
+    """BASELINE.json configs[4]: ipm_step_pcg on config-5 systems (n=2000 (3,6) code, one random
+    odd cut per check, d log-uniform over 12 decades, r ~ N(0,1)), device-resident, timed with
+    CUDA events over `steps` calls after `warmup` calls.  Algorithmic bytes per PCG iteration
+    B_min(p=1000, n_act=2000, m=1000) = 79,000 B."""
+    import torch
+    import paper_0902_0657_b200 as alp
+    from synth import config_code, c5_systems
+    code = config_code(5)
+    S = args.step_systems
+    sy = c5_systems(range(S), code)
+    c = alp.Code.from_synth(code)
+    masks = torch.from_numpy(sy.masks.view(np.int16)).to(dev)
+    d = torch.from_numpy(sy.d).to(dev)
+    r = torch.from_numpy(sy.r).to(dev)
+    res = None
+    for _ in range(max(1, args.warmup)):
+        res = alp.ipm_step_pcg(c, masks, d, r, stream=stream)
+    torch.cuda.synchronize(dev)
+    ms = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        res = alp.ipm_step_pcg(c, masks, d, r, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms.append(a.elapsed_time(b))
+    t = sum(ms) / len(ms) / 1e3
+    its = int(res.iters.sum().item())
+    st = res.status.cpu().numpy()
+    bmin = 8.0 * (code.n + code.m) + 48.0 * code.m + 5.0 * code.m + 2.0 * code.m
+    peak, kind = measured_peak_hbm()
+    gbs = its * bmin / t / 1e9
+    return {"workload": f"C5: {S} systems A D^2 A^T dy = r, (3,6) n=2000 m=1000, d = 10^U(-6,6), "
+                        "column-wise MTS PCG to true rel. residual 1e-8",
+            "systems_per_s": S / t, "ms_per_call": 1e3 * t, "pcg_iters_per_s": its / t,
+            "mean_pcg_iters": its / S, "status_counts": {int(k): int(v) for k, v in zip(*np.unique(st, return_counts=True))},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "bytes": "PCG iterations x B_min(1000, 2000, 1000) = 79 KB", "peak_kind": kind}}
 
 
 def main():

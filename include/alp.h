@@ -85,7 +85,7 @@ typedef enum {
 
 typedef struct alp_code alp_code;   /* opaque, immutable after creation */
 
-/* Per-frame counters (alp_decode) — 80 bytes.  cyc_* are SM clock cycles (clock64) the
+/* Per-frame counters (alp_decode) — 96 bytes.  cyc_* are SM clock cycles (clock64) the
  * frame's warp spent per phase: cut search + sign tables, IPM body (residuals, rhs,
  * Newton recovery, update), preconditioner build (sort, Alg. 7 peel, level schedule),
  * PCG SpMV, PCG preconditioner sweeps, remaining PCG work (axpys, dots, true residual). */
@@ -97,6 +97,7 @@ typedef struct {
   double g_max;        /* max_i min(u_i, 1 - u_i) of the output (integrality, C-11)       */
   double pcg_bytes;    /* sum over PCG iterations of B_min(p, n_act, m)    */
   int64_t cyc_cut, cyc_ipm, cyc_build, cyc_spmv, cyc_sweep, cyc_pcg_other;
+  int64_t cyc_sort, cyc_peel;   /* parts of cyc_build: column sort, Alg. 7 peel */
 } alp_frame_stats;
 
 typedef struct {

@@ -26,6 +26,7 @@ class FrameStats(C.Structure):
         ("max_p", C.c_int32), ("g_max", C.c_double), ("pcg_bytes", C.c_double),
         ("cyc_cut", C.c_int64), ("cyc_ipm", C.c_int64), ("cyc_build", C.c_int64),
         ("cyc_spmv", C.c_int64), ("cyc_sweep", C.c_int64), ("cyc_pcg_other", C.c_int64),
+        ("cyc_sort", C.c_int64), ("cyc_peel", C.c_int64),
     ]
 
 
@@ -33,8 +34,9 @@ class FrameStats(C.Structure):
 STATS_FIELDS = [("lp_solves", "<i4"), ("ipm_iters", "<i4"), ("pcg_iters", "<i4"),
                 ("max_p", "<i4"), ("g_max", "<f8"), ("pcg_bytes", "<f8"),
                 ("cyc_cut", "<i8"), ("cyc_ipm", "<i8"), ("cyc_build", "<i8"),
-                ("cyc_spmv", "<i8"), ("cyc_sweep", "<i8"), ("cyc_pcg_other", "<i8")]
-STATS_BYTES = 80
+                ("cyc_spmv", "<i8"), ("cyc_sweep", "<i8"), ("cyc_pcg_other", "<i8"),
+                ("cyc_sort", "<i8"), ("cyc_peel", "<i8")]
+STATS_BYTES = 96
 
 P = C.c_void_p
 SIGNATURES = {

@@ -114,7 +114,7 @@ class DecodeResult:
     objective: torch.Tensor   # [F] float64
     certificate: torch.Tensor  # [F] uint8
     status: torch.Tensor      # [F] int32
-    stats: torch.Tensor       # [F, 80] uint8 (alp_frame_stats); see stats_numpy()
+    stats: torch.Tensor       # [F, 96] uint8 (alp_frame_stats); see stats_numpy()
     u: torch.Tensor | None = None
     y: torch.Tensor | None = None
     masks: torch.Tensor | None = None

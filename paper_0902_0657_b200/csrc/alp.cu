@@ -364,6 +364,8 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
       st.cyc_spmv = F.cyc[CY_SPMV];
       st.cyc_sweep = F.cyc[CY_SWEEP];
       st.cyc_pcg_other = F.cyc[CY_PCG];
+      st.cyc_sort = F.cyc[CY_SORT];
+      st.cyc_peel = F.cyc[CY_PEEL];
       O.stats[f] = st;
     }
   }

@@ -86,7 +86,7 @@ __device__ __forceinline__ int wmaxi(int v) {
 }
 
 // Phase clock: lane 0 adds the cycles since `t` to counter `ph` and restarts `t`.
-enum { CY_CUT = 0, CY_IPM = 1, CY_BUILD = 2, CY_SPMV = 3, CY_SWEEP = 4, CY_PCG = 5 };
+enum { CY_CUT = 0, CY_IPM = 1, CY_BUILD = 2, CY_SPMV = 3, CY_SWEEP = 4, CY_PCG = 5, CY_SORT = 6, CY_PEEL = 7 };
 #define ALP_TICK(F, ph, t)                          \
   do {                                              \
     long long now_ = clock64();                     \
@@ -593,8 +593,15 @@ __device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* of
 __device__ void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
+  long long t0 = clock64();
   sort_columns(F);
+  long long t1 = clock64();
   peel_columnwise(F, p);
+  long long t2 = clock64();
+  if (F.lane == 0) {
+    F.cyc[CY_SORT] += t1 - t0;
+    F.cyc[CY_PEEL] += t2 - t1;
+  }
   uint16_t* poc = F.S<uint16_t>(L.s_poc);
   const uint16_t* prow = F.S<uint16_t>(L.s_prow);
   const uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
@@ -689,12 +696,13 @@ __device__ __forceinline__ int rec_at(const RecB& r, int k) {   // k compile-tim
 
 // Back substitution A_M f = r over the level schedule (P:585 stage 1): r in s_r, f in s_f,
 // both indexed by pivot row; f_R is the component of row R's pivot column.
+template <int DCT>
 __device__ __forceinline__ void back_step(const RecB& rec, const double* rS, double* fS) {
   const int head = rec_at(rec, 0);
   const int R = head & 0xffffff, nd = (head >> 24) & 0xf;
   double acc = rS[R];
 #pragma unroll
-  for (int d = 0; d < DCMAX; ++d) {
+  for (int d = 0; d < DCT - 1; ++d) {
     if (d < nd) {
       int dep = rec_at(rec, 1 + d);
       double fv = fS[dep & 0x7fffffff];
@@ -722,11 +730,11 @@ __device__ __forceinline__ void back_sweep(const Frame& F, int nLb) {
     RecB nxt;
     const bool hn = (lvl + 1 < nLb) && (b + F.lane < c);
     if (hn) load_recB(F.recB + (size_t)(b + F.lane) * RB, RB, nxt);
-    if (hc) back_step(cur, rS, fS);
+    if (hc) back_step<DCMAX + 1>(cur, rS, fS);
     for (int s = a + F.lane + 32; s < b; s += 32) {
       RecB t;
       load_recB(F.recB + (size_t)s * RB, RB, t);
-      back_step(t, rS, fS);
+      back_step<DCMAX + 1>(t, rS, fS);
     }
     __syncwarp();
     a = b;
@@ -735,6 +743,7 @@ __device__ __forceinline__ void back_sweep(const Frame& F, int nLb) {
     hc = hn;
   }
 }
+
 
 // Forward substitution A_M^T z = D_M^-2 f (P:585 stages 2-3); returns this lane's part of
 // z^T r = f^T D_M^-2 f (a sum of squares).
@@ -833,6 +842,51 @@ struct PcgResult {
 // shared memory (absent rows hold 0).  Returns h^T Q h accumulated as the sum of squares
 // sum_i d2_i (A^T h)_i^2 + sum_j d2_{n+j} h_j^2, so it is never <= 0 by cancellation.
 // With ABS, computes |A| D^2 |A|^T |h| instead (the rounding-floor estimate) and returns 0.
+// check pass of spmv: l_j = sum_i A_ji t_i + d2_{n+j} h_j, two checks per lane per step,
+// DCT >= the code's maximum check degree (compile-time, so the gathers unroll exactly)
+template <bool ABS, int DCT>
+__device__ __forceinline__ double spmv_checks(const Frame& F, const double* hS, const double* tS) {
+  const DCode& C = *F.C;
+  double hl = 0.0;
+  for (int j0 = F.lane; j0 < C.m; j0 += 64) {
+    uint16_t sc[2];
+    double hj[2], d2s[2];
+    int in[2][DCT];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = j0 + 32 * u;
+      const bool ok = j < C.m;
+      sc[u] = ok ? F.sgnC[j] : (uint16_t)0;
+      const int deg = ok ? (int)C.chk_deg[j] : 0;
+      hj[u] = ok ? hS[j] : 0.0;
+      d2s[u] = ok ? F.d2[C.n + j] : 0.0;
+#pragma unroll
+      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? chk_nb(C, j, t) : -1;
+    }
+    double acc[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double ds = d2s[u] * (ABS ? fabs(hj[u]) : hj[u]);
+      acc[u] = ds;
+#pragma unroll
+      for (int t = 0; t < DCT; ++t) {
+        if (in[u][t] >= 0) {
+          double tv = tS[in[u][t]];
+          if (ABS) acc[u] += tv;
+          else acc[u] = ((sc[u] >> t) & 1) ? acc[u] - tv : acc[u] + tv;
+        }
+      }
+      if (sc[u] & PRESENT) hl += hj[u] * ds;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = j0 + 32 * u;
+      if (j < C.m && (sc[u] & PRESENT)) F.l[j] = acc[u];
+    }
+  }
+  return hl;
+}
+
 template <bool ABS>
 __device__ __forceinline__ double spmv(const Frame& F) {
   const DCode& C = *F.C;
@@ -883,43 +937,10 @@ __device__ __forceinline__ double spmv(const Frame& F) {
     }
   }
   __syncwarp();
-  // check pass: l_j = sum_i A_ji t_i + d2_{n+j} h_j, two checks per lane per step
-  for (int j0 = F.lane; j0 < C.m; j0 += 64) {
-    uint16_t sc[2];
-    double hj[2], d2s[2];
-    int in[2][DCMAX];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = j0 + 32 * u;
-      const bool ok = j < C.m;
-      sc[u] = ok ? F.sgnC[j] : (uint16_t)0;
-      const int deg = ok ? (int)C.chk_deg[j] : 0;
-      hj[u] = ok ? hS[j] : 0.0;
-      d2s[u] = ok ? F.d2[C.n + j] : 0.0;
-#pragma unroll
-      for (int t = 0; t < DCMAX; ++t) in[u][t] = (t < dcs && t < deg) ? chk_nb(C, j, t) : -1;
-    }
-    double acc[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const double ds = d2s[u] * (ABS ? fabs(hj[u]) : hj[u]);
-      acc[u] = ds;
-#pragma unroll
-      for (int t = 0; t < DCMAX; ++t) {
-        if (in[u][t] >= 0) {
-          double tv = tS[in[u][t]];
-          if (ABS) acc[u] += tv;
-          else acc[u] = ((sc[u] >> t) & 1) ? acc[u] - tv : acc[u] + tv;
-        }
-      }
-      if (sc[u] & PRESENT) hl += hj[u] * ds;
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = j0 + 32 * u;
-      if (j < C.m && (sc[u] & PRESENT)) F.l[j] = acc[u];
-    }
-  }
+  // check pass, specialised on the maximum check degree so the unrolled gathers match it
+  if (dcs <= 6) hl += spmv_checks<ABS, 6>(F, hS, tS);
+  else if (dcs <= 12) hl += spmv_checks<ABS, 12>(F, hS, tS);
+  else hl += spmv_checks<ABS, DCMAX>(F, hS, tS);
   __syncwarp();
   return ABS ? 0.0 : wsum(hl);
 }

@@ -21,11 +21,13 @@ for fps in [int(v) for v in os.environ.get("FPS", "12,8,6,4,3").split(",")]:
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
     st = res.stats_numpy()
-    cyc = {k: float(st[k].sum()) for k in ("cyc_cut", "cyc_ipm", "cyc_build", "cyc_spmv", "cyc_sweep", "cyc_pcg_other")}
+    cyc = {k: float(st[k].sum()) for k in ("cyc_cut", "cyc_ipm", "cyc_build", "cyc_spmv", "cyc_sweep", "cyc_pcg_other", "cyc_sort", "cyc_peel")}
     its = st["pcg_iters"].sum()
     obj = res.objective.cpu().numpy()
     same = "n/a" if ref is None else ("%.1e" % np.max(np.abs(obj - ref) / np.maximum(1, np.abs(ref))))
     ref = obj if ref is None else ref
-    print("fps %2d: %.3f s  %.0f frames/s | per PCG it: spmv %.0f sweep %.0f other %.0f cyc | build/IPM-it %.0f | ipm-body/IPM-it %.0f | obj diff %s" % (
+    print("fps %2d: %.3f s  %.0f frames/s | per PCG it: spmv %.0f sweep %.0f other %.0f cyc | per IPM it: build %.0f (sort %.0f peel %.0f) body %.0f, PCG its/IPM it %.1f | obj diff %s" % (
         fps, dt, F / dt, cyc["cyc_spmv"] / its, cyc["cyc_sweep"] / its, cyc["cyc_pcg_other"] / its,
-        cyc["cyc_build"] / st["ipm_iters"].sum(), cyc["cyc_ipm"] / st["ipm_iters"].sum(), same), flush=True)
+        cyc["cyc_build"] / st["ipm_iters"].sum(), cyc["cyc_sort"] / st["ipm_iters"].sum(),
+        cyc["cyc_peel"] / st["ipm_iters"].sum(), cyc["cyc_ipm"] / st["ipm_iters"].sum(),
+        its / st["ipm_iters"].sum(), same), flush=True)
