@@ -75,8 +75,10 @@ typedef enum {
   ALP_FRAME_PCG_BREAKDOWN = 8,   /* some PCG solve met h^T Q h <= 0 (or non-finite)          */
   ALP_FRAME_NUMERIC = 16,        /* non-finite IPM iterate; decoding of the frame stopped   */
   ALP_FRAME_PCG_FLOOR = 32,      /* informational: some PCG solve stopped with its TRUE
-                                    residual at the fp64 evaluation floor
-                                    16 eps || |A| D^2 |A|^T |dy| ||_2, above pcg_rel_tol ||w|| */
+                                    residual above pcg_rel_tol ||w|| at the fp64 attainable
+                                    accuracy: at most the evaluation floor f = 16 eps
+                                    || |A| D^2 |A|^T |dy| ||_2, or within 1e3 f with restarts
+                                    (iterative refinement) no longer halving it          */
   ALP_FRAME_PCG_FALLBACK = 64    /* informational: some MTS-preconditioned PCG run broke down
                                     or failed the true-residual test, and the solve was redone
                                     by Jacobi-preconditioned CG; the better result was kept

@@ -372,15 +372,23 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layout L, char* slots,
+__global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
+                                                        char* slots,
                                                         const double* __restrict__ llr,
                                                         long long n_frames, DecodeOut O,
                                                         int* counter) {
   extern __shared__ __align__(16) char smem[];
+  __shared__ DCode sC;    // code / layout descriptors in shared memory: the Frame's pointers to
+  __shared__ Layout sL;   // them must not land in local memory
+  if (threadIdx.x == 0) sL = L;
+  DCode Cs;
+  stage_graph(C, G, smem, Cs);
+  if (threadIdx.x == 0) sC = Cs;
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   Frame F;
-  frame_bind(F, &C, &L, slots + gw * L.slot_bytes, smem + warp * L.smem_bytes, lane);
+  frame_bind(F, &sC, &sL, slots + gw * L.slot_bytes, smem + G.bytes + warp * L.smem_bytes, lane);
   while (true) {
     long long f = 0;
     if (lane == 0) f = atomicAdd(counter, 1);
@@ -404,13 +412,21 @@ struct StepIO {
 };
 
 // Isolated step solve (eq.`Delta y` P:479) per system: signs, D^2, Alg. 7, PCG.
-__global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout L, char* slots,
-                                                      long long n_sys, StepIO io, int* counter) {
+__global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout L, GraphSmem G,
+                                                      char* slots, long long n_sys, StepIO io,
+                                                      int* counter) {
   extern __shared__ __align__(16) char smem[];
+  __shared__ DCode sC;
+  __shared__ Layout sL;
+  if (threadIdx.x == 0) sL = L;
+  DCode Cs;
+  stage_graph(C, G, smem, Cs);
+  if (threadIdx.x == 0) sC = Cs;
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   Frame F;
-  frame_bind(F, &C, &L, slots + gw * L.slot_bytes, smem + warp * L.smem_bytes, lane);
+  frame_bind(F, &sC, &sL, slots + gw * L.slot_bytes, smem + G.bytes + warp * L.smem_bytes, lane);
   const int n = C.n, m = C.m, Q = C.Q;
   while (true) {
     long long s = 0;
@@ -607,6 +623,24 @@ Layout make_layout(const DCode& C, int smem_budget) {
   return L;
 }
 
+GraphSmem make_graph_smem(const DCode& C) {
+  GraphSmem G;
+  size_t o = 0;
+  auto a = [&](size_t bytes) {
+    size_t r = o;
+    o += al(bytes, 16);
+    return (int)r;
+  };
+  G.o_chk_var = a(2 * (size_t)C.m * C.dc);
+  G.o_chk_deg = a(C.m);
+  G.o_var_chk = a(2 * (size_t)C.n * C.dv);
+  G.o_var_slot = a((size_t)C.n * C.dv);
+  G.o_var_deg = a(C.n);
+  G.bytes = (int)al(o, 128);
+  if (G.bytes > 48 * 1024) G = GraphSmem{0, 0, 0, 0, 0, 0};   // large codes: graph stays global
+  return G;
+}
+
 // Shared-memory budget per warp (frame): the device's per-block opt-in limit split over
 // `frames_per_sm` resident frames.
 int smem_budget_for(const alp_params* p) {
@@ -659,7 +693,8 @@ struct LaunchCfg {
 };
 
 template <class K>
-alp_status plan_launch(K kernel, const Layout& L, long long units, const alp_params* p, LaunchCfg& cfg) {
+alp_status plan_launch(K kernel, const Layout& L, int graph_bytes, long long units, const alp_params* p,
+                       LaunchCfg& cfg) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -667,12 +702,13 @@ alp_status plan_launch(K kernel, const Layout& L, long long units, const alp_par
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  smem_optin -= 1024;   // static shared memory of the kernels (code / layout descriptors)
   int wpb = (p && p->warps_per_block > 0) ? p->warps_per_block : 4;
-  while (wpb > 1 && (long long)wpb * L.smem_bytes > smem_optin) --wpb;
-  if ((long long)wpb * L.smem_bytes > smem_optin)
+  while (wpb > 1 && (long long)wpb * L.smem_bytes + graph_bytes > smem_optin) --wpb;
+  if ((long long)wpb * L.smem_bytes + graph_bytes > smem_optin)
     return fail(ALP_ERR_UNSUPPORTED, "per-frame shared memory " + std::to_string(L.smem_bytes) +
                                          " B exceeds the device limit");
-  int smem_block = wpb * L.smem_bytes;
+  int smem_block = wpb * L.smem_bytes + graph_bytes;
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_block);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   int nb = 0;
@@ -794,7 +830,10 @@ alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const i
   c->E = E;
   cudaError_t e;
   auto up = [&](void** dst, const void* src, size_t bytes) -> bool {
-    e = cudaMalloc(dst, bytes);
+    const size_t padded = al(bytes, 16);   // the kernels stage these arrays with 4-byte loads
+    e = cudaMalloc(dst, padded);
+    if (e != cudaSuccess) return false;
+    e = cudaMemset(*dst, 0, padded);
     if (e != cudaSuccess) return false;
     e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
     return e == cudaSuccess;
@@ -835,7 +874,7 @@ size_t alp_decode_workspace_bytes(const alp_code* code, int64_t n_frames, const 
   DCode C = make_dcode(code);
   Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
-  if (plan_launch(alp_decode_kernel, L, std::max<int64_t>(n_frames, 1), params, cfg) != ALP_OK) return 0;
+  if (plan_launch(alp_decode_kernel, L, make_graph_smem(C).bytes, std::max<int64_t>(n_frames, 1), params, cfg) != ALP_OK) return 0;
   return kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
 }
 
@@ -847,7 +886,7 @@ size_t alp_pcg_workspace_bytes(const alp_code* code, int64_t n_sys, const alp_pa
   DCode C = make_dcode(code);
   Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
-  if (plan_launch(pcg_step_kernel, L, std::max<int64_t>(n_sys, 1), params, cfg) != ALP_OK) return 0;
+  if (plan_launch(pcg_step_kernel, L, make_graph_smem(C).bytes, std::max<int64_t>(n_sys, 1), params, cfg) != ALP_OK) return 0;
   return kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
 }
 
@@ -869,7 +908,8 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
   DCode C = make_dcode(code);
   Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
-  alp_status st = plan_launch(alp_decode_kernel, L, n_frames, params, cfg);
+  const GraphSmem G = make_graph_smem(C);
+  alp_status st = plan_launch(alp_decode_kernel, L, G.bytes, n_frames, params, cfg);
   if (st != ALP_OK) return st;
   size_t need = kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
   if (workspace_bytes < need)
@@ -880,7 +920,7 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   DecodeOut O{hard, objective, certificate, frame_status, stats, u_out, y_out, mask_out};
   alp_decode_kernel<<<cfg.grid, 32 * cfg.wpb, cfg.smem_block, s>>>(
-      C, make_params(params), L, (char*)workspace + kCounterBytes, llr, (long long)n_frames, O, counter);
+      C, make_params(params), L, G, (char*)workspace + kCounterBytes, llr, (long long)n_frames, O, counter);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "alp_decode_kernel launch");
   g_last_launches = 1;
@@ -960,7 +1000,8 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   DCode C = make_dcode(code);
   Layout L = make_layout(C, smem_budget_for(params));
   LaunchCfg cfg;
-  alp_status st = plan_launch(pcg_step_kernel, L, n_sys, params, cfg);
+  const GraphSmem G = make_graph_smem(C);
+  alp_status st = plan_launch(pcg_step_kernel, L, G.bytes, n_sys, params, cfg);
   if (st != ALP_OK) return st;
   size_t need = kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
   if (workspace_bytes < need)
@@ -971,7 +1012,7 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   StepIO io{masks, flip, d, r, dy, pcg_iters, rel_res, sys_status, pivot_rows, pivot_cols};
   pcg_step_kernel<<<cfg.grid, 32 * cfg.wpb, cfg.smem_block, s>>>(
-      C, make_params(params), L, (char*)workspace + kCounterBytes, (long long)n_sys, io, counter);
+      C, make_params(params), L, G, (char*)workspace + kCounterBytes, (long long)n_sys, io, counter);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pcg_step_kernel launch");
   g_last_launches = 1;

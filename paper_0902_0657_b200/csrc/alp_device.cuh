@@ -40,6 +40,33 @@ struct DCode {
   const uint8_t* __restrict__ var_deg;    // [n]
 };
 
+// Per-CTA shared copy of the Tanner graph (host-computed byte offsets; 0 bytes = stay global).
+struct GraphSmem {
+  int bytes, o_chk_var, o_chk_deg, o_var_chk, o_var_slot, o_var_deg;
+};
+
+// Every thread of the CTA copies the graph arrays into the CTA's shared area `g` and gets a
+// DCode whose pointers address that copy (graph reads become shared-memory loads).
+__device__ __forceinline__ void stage_graph(const DCode& C, const GraphSmem& G, char* g, DCode& out) {
+  out = C;
+  if (G.bytes == 0) return;
+  auto cp = [&](const void* src, int off, int bytes) {
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d4 = reinterpret_cast<uint32_t*>(g + off);
+    for (int k = threadIdx.x; k < (bytes + 3) / 4; k += blockDim.x) d4[k] = s4[k];
+  };
+  cp(C.chk_var, G.o_chk_var, C.m * C.dc * 2);
+  cp(C.chk_deg, G.o_chk_deg, C.m);
+  cp(C.var_chk, G.o_var_chk, C.n * C.dv * 2);
+  cp(C.var_slot, G.o_var_slot, C.n * C.dv);
+  cp(C.var_deg, G.o_var_deg, C.n);
+  out.chk_var = reinterpret_cast<const uint16_t*>(g + G.o_chk_var);
+  out.chk_deg = reinterpret_cast<const uint8_t*>(g + G.o_chk_deg);
+  out.var_chk = reinterpret_cast<const uint16_t*>(g + G.o_var_chk);
+  out.var_slot = reinterpret_cast<const uint8_t*>(g + G.o_var_slot);
+  out.var_deg = reinterpret_cast<const uint8_t*>(g + G.o_var_deg);
+}
+
 // Byte offsets inside one warp's global slot and shared-memory window (host-computed).
 struct Layout {
   long long slot_bytes;
@@ -163,11 +190,11 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
 }
 
 __device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
-  const unsigned v = __ldg(C.chk_var + j * C.dc + t);
+  const unsigned v = C.chk_var[j * C.dc + t];
   return v == 0xffffu ? -1 : (int)v;
 }
 __device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
-  const unsigned v = __ldg(C.var_chk + i * C.dv + k);
+  const unsigned v = C.var_chk[i * C.dv + k];
   return v == 0xffffu ? -1 : (int)v;
 }
 
@@ -310,17 +337,31 @@ __device__ void sort_columns(const Frame& F) {
     keys[c] = k;
   }
   __syncwarp();
-  const int N = C.QP2;
+  const int N = C.QP2;   // power of two >= 64
+  // Bitonic network; each lane's compare-exchanges of a stage are independent, so they are
+  // done four at a time with all eight loads issued before any store (latency overlap).
   for (int k = 2; k <= N; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = F.lane; t < (N >> 1); t += 32) {
-        int lo = 2 * j * (t / j) + (t % j);
-        int hi = lo + j;
-        bool up = ((lo & k) == 0);
-        uint64_t a = keys[lo], b = keys[hi];
-        if ((a > b) == up) {
-          keys[lo] = b;
-          keys[hi] = a;
+      for (int t0 = F.lane; t0 < (N >> 1); t0 += 128) {
+        int lo[4], hi[4];
+        uint64_t a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + 32 * u;
+          lo[u] = 2 * j * (t / j) + (t % j);
+          hi[u] = lo[u] + j;
+          const bool ok = t < (N >> 1);
+          a[u] = ok ? keys[lo[u]] : 0ull;
+          b[u] = ok ? keys[hi[u]] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + 32 * u;
+          const bool up = ((lo[u] & k) == 0);
+          if (t < (N >> 1) && (a[u] > b[u]) == up) {
+            keys[lo[u]] = b[u];
+            keys[hi[u]] = a[u];
+          }
         }
       }
       __syncwarp();
@@ -950,7 +991,8 @@ __device__ __forceinline__ double spmv(const Frame& F) {
 // then evaluated and must pass the same test.  Outcomes: 0 converged, ST_PCG_FLOOR (true
 // residual at the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||), ST_PCG_MAXITER,
 // ST_PCG_BREAKDOWN (h^T Q h or z^T r not > 0 / non-finite, the recursive residual
-// diverging 1e8-fold, or — MTS mode — no new minimum in 200 iterations).  When the
+// diverging 1e8-fold, or — MTS mode — no new minimum in 200 iterations).  ST_PCG_FLOOR also
+// ends a refinement restart that no longer halves the true residual within 1e3x of the floor.  When the
 // recursion converges but the true residual fails the test, the run restarts from the
 // true residual (iterative refinement with the same preconditioner), at most 4 times.
 // `it` accumulates iterations across runs.
@@ -973,6 +1015,7 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
   }
   __syncwarp();
   relres = 1.0;
+  double prev_trn = 1e308;
   for (int restart = 0; restart <= 4; ++restart) {
     double rz;
     precond_apply(F, mode, nLb, nLf, rz);   // line 3
@@ -1067,9 +1110,15 @@ __device__ int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int n
     for (int j = F.lane; j < C.m; j += 32)
       if (F.sgnC[j] & PRESENT) aa += F.l[j] * F.l[j];
     aa = sqrt(wsum(aa));
-    if (trn <= 16.0 * 2.220446049250313e-16 * aa) return ST_PCG_FLOOR;
+    const double floor_est = 16.0 * 2.220446049250313e-16 * aa;
+    if (trn <= floor_est) return ST_PCG_FLOOR;
     if (!conv) return ST_PCG_MAXITER;
-    // the recursion converged but the true residual did not: restart from it
+    // The recursion converged but the true residual did not: restart from it (iterative
+    // refinement with the same preconditioner).  A restart that does not halve the true
+    // residual while it is within 1e3x of the evaluation-floor estimate has reached the
+    // attainable fp64 accuracy: stop there (ST_PCG_FLOOR).
+    if (trn > 0.5 * prev_trn && trn <= 1e3 * floor_est) return ST_PCG_FLOOR;
+    prev_trn = trn;
   }
   return ST_PCG_MAXITER;
 }

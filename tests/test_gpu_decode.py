@@ -56,7 +56,9 @@ def compare(code, llr, g, frames, variant="A"):
         assert np.array_equal(g["hard"][f][sure], o["hard"][sure]), f"frame {f}: hard decisions differ"
         if abs(o["g_max"] - 1e-2) > 1e-3:
             assert g["cert"][f] == o["cert"], f"frame {f}: certificate differs"
-        assert abs(g["obj"][f] - o["obj"]) <= 1e-6 * max(1.0, abs(o["obj"])), \
+        # P3 on the cost scale: the IPM stop (C-8) is relative to (1 + |c^T x|) and ||c||inf
+        scale = max(1.0, abs(o["obj"]), float(np.max(np.abs(llr[f]))))
+        assert abs(g["obj"][f] - o["obj"]) <= 1e-6 * scale, \
             f"frame {f}: objective {g['obj'][f]} vs {o['obj']}"
         lp_match += int(g["stats"]["lp_solves"][f] == o["lp_solves"])
     return dict(lp_match=lp_match / max(1, len(frames)))

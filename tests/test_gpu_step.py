@@ -71,9 +71,9 @@ def _check_system(code, mk, dd, rr, fl, out, s, tol_dy=1e-8, check_pivots=True):
     floor = 16 * EPS * np.linalg.norm(np.abs(A) @ (w2 * (np.abs(A).T @ np.abs(got)))) / wn
     if not st & FLOOR:
         assert out["relres"][s] <= 1e-8
-    else:
-        assert out["relres"][s] <= 1.01 * floor
-    assert tres <= 1.5 * max(1e-8, floor), f"system {s}: true residual {tres:.3e}"
+    else:   # attainable-accuracy stop: within 1e3x of the evaluation floor (include/alp.h)
+        assert out["relres"][s] <= 1.01e3 * floor
+    assert tres <= 1.5 * max(1e-8, 1e3 * floor if st & FLOOR else floor), f"system {s}: true residual {tres:.3e}"
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert err <= tol_dy, f"system {s}: rel err {err:.3e}"
     absent = [j for j in range(code.m) if j not in set(rows)]
