@@ -40,7 +40,7 @@ struct IpmOut {
 // Arrays: v holds r_c then D^2 r_c - Z^-1 r_e then dx; d2 holds D^2 then dz; w holds r_b
 // then the PCG right-hand side.
 // =====================================================================================
-__device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
+__device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
                             double bmax, double cmax, long long frame_id, int lp_id) {
   const DCode& C = *F.C;
   const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
@@ -73,7 +73,7 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
   int it = 0;
   while (true) {
     double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
-#pragma unroll 2
+#pragma unroll 4
     for (int j = lane; j < m; j += 32) {
       uint16_t s = SC[j];
       if (!(s & PRESENT)) continue;
@@ -130,7 +130,7 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
       V[c] = d2 * V[c] - re / zc;
     }
     __syncwarp();
-#pragma unroll 2
+#pragma unroll 4
     for (int j = lane; j < m; j += 32) {
       uint16_t s = SC[j];
       if (!(s & PRESENT)) continue;
@@ -152,7 +152,7 @@ __device__ IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, in
     // well below z ~ mu on the basic columns, so late in the IPM the recursion runs to
     // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); acceptance stays ||w - Q dy|| <= 1e-8||w||
     const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, 1e-2 * mu));
-    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, inner);
+    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, inner, 1e-6);
     tk = clock64();
 
     out.status |= pr.status;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
           if (io.pcol) io.pcol[s * m + k] = -1;
         }
     }
-    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, P.pcg_rel_tol);
+    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, P.pcg_rel_tol, 1.0);
     for (int j = lane; j < m; j += 32) io.dy[s * m + j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
     if (lane == 0) {
       if (io.iters) io.iters[s] = pr.iters;
