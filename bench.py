@@ -318,6 +318,14 @@ def run_ours(args):
     peak, peak_kind = measured_peak_hbm()
     # dominant (only) kernel: alp_decode_kernel, one launch per step on `stream`
     achieved = pcg_bytes / (t_rank / args.steps) / 1e9
+    traffic, traffic_src = None, None
+    try:   # DRAM bytes per frame from the committed ncu --set full capture, scaled to this launch
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tj = json.load(fh)
+        traffic = float(tj["dram_bytes_per_frame"]) * F
+        traffic_src = f"{tj['capture']}: {tj['frames']} frames, scaled per frame to {F}"
+    except (OSError, KeyError, ValueError):
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
@@ -326,7 +334,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": pcg_bytes,
                      "kernel": "alp_decode_kernel",
                      "bytes": "sum over executed PCG iterations of B_min(p,n_act,m) (DESIGN.md §6)",
                      "peak_kind": peak_kind},

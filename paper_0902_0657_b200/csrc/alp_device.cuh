@@ -331,20 +331,30 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
 __device__ ALP_HEAVY void sort_columns(const Frame& F) {
   const DCode& C = *F.C;
   uint64_t* keys = F.S<uint64_t>(F.L->s_keys);
-  for (int c = F.lane; c < C.QP2; c += 32) {
+  // valid columns (>= 1 present row) are compacted to the front (warp ballot prefix), the rest
+  // of the key array is padding (~0); only the next power of two >= #valid is sorted
+  int nv = 0;
+  const unsigned lt = (1u << F.lane) - 1u;
+  for (int c0 = 0; c0 < C.Q; c0 += 32) {
+    const int c = c0 + F.lane;
+    bool valid = false;
     uint64_t k = ~0ull;
     if (c < C.Q) {
-      bool valid = (c < C.n) ? ((F.sgnV[c] & 0xf) != 0) : ((F.sgnC[c - C.n] & PRESENT) != 0);
+      valid = (c < C.n) ? ((F.sgnV[c] & 0xf) != 0) : ((F.sgnC[c - C.n] & PRESENT) != 0);
       if (valid) {
         float f = __double2float_rn(F.d2[c]);  // monotone non-decreasing map
         uint32_t fb = __float_as_uint(f) & 0x7fffffffu;
         k = ((uint64_t)(~fb) << 32) | (uint32_t)c;
       }
     }
-    keys[c] = k;
+    const unsigned bal = __ballot_sync(FULL, valid);
+    if (valid) keys[nv + __popc(bal & lt)] = k;
+    nv += __popc(bal);
   }
+  int N = 64;
+  while (N < nv) N <<= 1;
+  for (int c = nv + F.lane; c < C.QP2; c += 32) keys[c] = ~0ull;
   __syncwarp();
-  const int N = C.QP2;   // power of two >= 64
   // Bitonic network; each lane's compare-exchanges of a stage are independent, so they are
   // done four at a time with all eight loads issued before any store (latency overlap).
   for (int k = 2; k <= N; k <<= 1) {
