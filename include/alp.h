@@ -123,7 +123,7 @@ typedef struct {
   int32_t warps_per_block;/* tuning: frames (one warp each) per CTA; 0 = automatic             */
   int32_t smem_frames_per_sm; /* tuning: resident frames per SM the shared-memory budget is split
                              over; hot PCG arrays move into shared memory while they fit;
-                             0 = automatic (12: measured best, a small window keeps L1 large) */
+                             0 = automatic (11: measured best; a small window keeps L1 large) */
 } alp_params;
 
 /* Fills the defaults listed above (identical to the oracle's constants). */

@@ -648,7 +648,7 @@ int smem_budget_for(const alp_params* p) {
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
     optin = 227 * 1024;
-  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 12;
+  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 11;
   return (optin / fps) & ~127;
 }
 

@@ -351,7 +351,7 @@ __device__ ALP_HEAVY void sort_columns(const Frame& F) {
     if (valid) keys[nv + __popc(bal & lt)] = k;
     nv += __popc(bal);
   }
-  int N = 64;
+  int N = 1;   // power of two >= #valid (<= QP2, the key array's length)
   while (N < nv) N <<= 1;
   for (int c = nv + F.lane; c < C.QP2; c += 32) keys[c] = ~0ull;
   __syncwarp();
