@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
+    ap.add_argument("--snr-sweep", type=int, default=1,
+                    help="also decode the config's other SNRs (2.0, 2.5 dB) once each and report them")
     ap.add_argument("--step-systems", type=int, default=65536,
                     help="config-5 isolated step solves timed beside the decode (0 = skip)")
     return ap.parse_args()
@@ -350,6 +352,27 @@ def run_ours(args):
     if not args.no_e2e:
         line["e2e"] = {"value": total_frames / e2e_max, "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if args.snr_sweep and ws == 1:
+        line["snr_sweep"] = {}
+        for si in range(len(SNRS)):
+            if si == args.snr_idx:
+                continue
+            fbs = config_frames(2, si, frames=frame_ids, code=code)
+            llr_s = torch.from_numpy(fbs.llr).to(dev)
+            alp.decode(c, llr_s, stream=stream, out=out)     # warm-up (same shapes)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.fill_(7)
+            a.record(stream)
+            alp.decode(c, llr_s, stream=stream, out=out)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            cs = frame_counters(out.hard.cpu().numpy(), fbs.codewords, out.certificate.cpu().numpy(),
+                                out.status.cpu().numpy(), out.stats_numpy())
+            stv = out.status.cpu().numpy()
+            line["snr_sweep"][f"{SNRS[si]} dB"] = {
+                "frames_per_s": F / (a.elapsed_time(b) / 1e3), "frame_errors": int(cs[1]),
+                "not_certified": int(cs[2]),
+                "frames_with_cap_status": int(((stv & ~96) != 0).sum())}
     if args.step_systems > 0:
         line["step_solve"] = time_step_solve(args, dev, stream)
     if ws == 1 and not args.no_cpu_baseline:

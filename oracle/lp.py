@@ -35,6 +35,7 @@ DEFAULT_PARAMS = dict(
     pcg_rel_tol=1e-8,
     tau_viol=1e-6, tau_act=1e-6, tau_cert=1e-2,
     alp_max_iter=200, ipm_max_iter=100, pcg_max_iter=1000,
+    stop_on_lp_failure=1,
 )
 
 # per-frame status bits (mirrors include/alp.h alp_frame_status)
@@ -397,7 +398,9 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
             trace.append(dict(pool={j: np.array(v) for j, v in pool.items()} if variant != "ALP"
                               else list(alp_rows), u=u.copy(), obj=objs[-1], p=lp["p"],
                               ipm_iters=res["iters"]))
-        if status & ST_NUMERIC:
+        if (status & ST_NUMERIC) or (P.get("stop_on_lp_failure", 1) and (res["status"] & ST_IPM_MAXITER)):
+            # reading C-30: an LP that did not converge gives no trustworthy u for the next
+            # cut search; the frame stops with its status bits and the last u
             break
     hard, obj, g_max, cert = decode_outputs(code, gamma, u, P["tau_cert"])
     masks = np.zeros(m, dtype=np.uint16)

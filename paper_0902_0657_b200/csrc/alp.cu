@@ -70,7 +70,7 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
   long long tk = clock64();
   // algorithmic bytes per PCG iteration of this LP
   const double Bmin = 8.0 * (nact + p) + 48.0 * p + 5.0 * p + 2.0 * m;
-  int it = 0;
+  int it = 0, bad_solves = 0;
   while (true) {
     double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
 #pragma unroll 4
@@ -156,6 +156,16 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     tk = clock64();
 
     out.status |= pr.status;
+    // three consecutive step solves that failed even after the fallback: the Newton direction
+    // is garbage and the IPM cannot progress; give the LP up as non-converged (C-30)
+    bad_solves = (pr.status & (ST_PCG_MAXITER | ST_PCG_BREAKDOWN)) ? bad_solves + 1 : 0;
+    if (bad_solves >= 3) {
+      out.status |= ST_IPM_MAXITER;
+      out.pcg_iters += pr.iters;
+      out.pcg_bytes += (double)pr.iters * Bmin;
+      it++;
+      break;
+    }
     if (g_trace) {
       double dmn = 1e308, dmx = 0.0;
       for (int c = lane; c < Q; c += 32) {
@@ -321,7 +331,10 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
     }
     __syncwarp();
     tk = clock64();
-    if (o.status & ST_NUMERIC) break;
+    // Reading C-30: an LP whose IPM ended on a non-finite iterate or at the Newton-step cap
+    // gives no trustworthy u for the next cut search, so the frame's decode stops there
+    // (status bits set, last u output; `stop_on_lp_failure = 0` keeps going).
+    if ((o.status & ST_NUMERIC) || (P.stop_on_lp_failure && (o.status & ST_IPM_MAXITER))) break;
   }
   ALP_TICK(F, CY_CUT, tk);
   // outputs: hard decision, objective gamma^T u, g_max, ML certificate
@@ -665,6 +678,7 @@ Params make_params(const alp_params* p) {
   P.feas_tol = p->feas_tol;
   P.pcg_rel_tol = p->pcg_rel_tol;
   P.pcg_fallback_tol = p->pcg_fallback_tol;
+  P.stop_on_lp_failure = p->stop_on_lp_failure;
   P.tau_viol = p->tau_viol;
   P.tau_act = p->tau_act;
   P.tau_cert = p->tau_cert;
@@ -749,6 +763,7 @@ void alp_default_params(alp_params* p) {
   p->pcg_max_iter = 1000;
   p->warps_per_block = 0;
   p->smem_frames_per_sm = 0;
+  p->stop_on_lp_failure = 1;
 }
 
 const char* alp_status_string(alp_status s) {

@@ -35,6 +35,7 @@ struct Params {
   int variant, precond;
   double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, pcg_fallback_tol, tau_viol, tau_act, tau_cert;
   int alp_max_iter, ipm_max_iter, pcg_max_iter;
+  int stop_on_lp_failure;
 };
 
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
