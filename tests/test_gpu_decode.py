@@ -185,3 +185,13 @@ def test_config2_full_batch_certified():
     g = gpu_decode(code, fb.llr)
     assert_certified(code, fb.llr, g, 0.99)
     compare(code, fb.llr, g, np.random.default_rng(1).choice(fb.F, 6, replace=False))
+
+
+def test_config1_plain_cg_decode():
+    """SURVEY f-1 baseline: the same decode with plain CG (precond = 1) instead of the
+    column-wise MTS preconditioner reaches the same LP outputs (P1-P3, P6)."""
+    code = config_code(1)
+    fb = config_frames(1, frames=range(32))
+    g = gpu_decode(code, fb.llr, precond=1)
+    assert_certified(code, fb.llr, g)
+    compare(code, fb.llr, g, range(8))
