@@ -1041,6 +1041,7 @@ __device__ ALP_HEAVY int pcg_run(const Frame& F, const Params& P, int mode, int 
     for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? zS[j] : 0.0;   // line 4
     __syncwarp();
     bool conv = false, bad = false;
+    int past = -1;
     double rrmin = 1e308;
     int since_min = 0;
     long long tk = clock64();
@@ -1073,6 +1074,15 @@ __device__ ALP_HEAVY int pcg_run(const Frame& F, const Params& P, int mode, int 
       if (sqrt(rr) <= itol) {
         conv = true;
         break;
+      }
+      // past the acceptance tolerance, the forcing-term target gets at most 50 more iterations
+      // (an unreachable target would otherwise let the recursion drift, R-1)
+      if (sqrt(rr) <= tol) {
+        if (past < 0) past = it;
+        else if (it - past >= 50) {
+          conv = true;
+          break;
+        }
       }
       if (rr < rrmin) {
         rrmin = rr;
