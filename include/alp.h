@@ -124,6 +124,8 @@ typedef struct {
   int32_t smem_frames_per_sm; /* tuning: resident frames per SM the shared-memory budget is split
                              over; hot PCG arrays move into shared memory while they fit;
                              0 = automatic (11: measured best; a small window keeps L1 large) */
+  int32_t pcg_fallback;   /* 1: MTS-PCG failures are redone by Jacobi CG (R-2); 0: report them
+                             as they are (diagnostics, e.g. residual traces)              1      */
   int32_t stop_on_lp_failure; /* 1: a frame stops decoding after an LP whose IPM hit
                              ipm_max_iter (reading C-30; status bit set, last u output)  1      */
 } alp_params;

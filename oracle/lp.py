@@ -35,7 +35,7 @@ DEFAULT_PARAMS = dict(
     pcg_rel_tol=1e-8,
     tau_viol=1e-6, tau_act=1e-6, tau_cert=1e-2,
     alp_max_iter=200, ipm_max_iter=100, pcg_max_iter=1000,
-    stop_on_lp_failure=1,
+    stop_on_lp_failure=1, pcg_fallback=1,
 )
 
 # per-frame status bits (mirrors include/alp.h alp_frame_status)

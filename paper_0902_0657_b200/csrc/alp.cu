@@ -679,6 +679,7 @@ Params make_params(const alp_params* p) {
   P.pcg_rel_tol = p->pcg_rel_tol;
   P.pcg_fallback_tol = p->pcg_fallback_tol;
   P.stop_on_lp_failure = p->stop_on_lp_failure;
+  P.pcg_fallback = p->pcg_fallback;
   P.tau_viol = p->tau_viol;
   P.tau_act = p->tau_act;
   P.tau_cert = p->tau_cert;
@@ -764,6 +765,7 @@ void alp_default_params(alp_params* p) {
   p->warps_per_block = 0;
   p->smem_frames_per_sm = 0;
   p->stop_on_lp_failure = 1;
+  p->pcg_fallback = 1;
 }
 
 const char* alp_status_string(alp_status s) {

@@ -35,7 +35,7 @@ struct Params {
   int variant, precond;
   double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, pcg_fallback_tol, tau_viol, tau_act, tau_cert;
   int alp_max_iter, ipm_max_iter, pcg_max_iter;
-  int stop_on_lp_failure;
+  int pcg_fallback, stop_on_lp_failure;
 };
 
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
@@ -1198,7 +1198,7 @@ __device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, in
   }
   double rel1 = 1.0;
   int st1 = pcg_run(F, P, PC_MTS, nLb, nLf, wn, it, P.pcg_max_iter, rel1, P.pcg_rel_tol, inner_tol);
-  if (st1 == 0 || (st1 == ST_PCG_FLOOR && rel1 <= floor_accept)) {   // converged / attainable
+  if (st1 == 0 || (st1 == ST_PCG_FLOOR && rel1 <= floor_accept) || !P.pcg_fallback) {
     res.status = st1;
     res.relres = rel1;
     res.iters = it;
