@@ -109,9 +109,11 @@ typedef struct {
   double eta;             /* step damping of the ratio test (C-6)                0.99   */
   double gap_tol;         /* stop: x^T z <= gap_tol * (1 + |c^T x|) (C-8)               1e-9   */
   double feas_tol;        /* stop: ||r_b||, ||r_c|| <= feas_tol * (1 + ||b||, ||c||)    1e-8   */
-  double pcg_rel_tol;     /* PCG stop: ||r||_2 <= pcg_rel_tol * ||w||_2 (C-9, G15) on the
-                             recursive residual, then verified on the TRUE residual
-                             w - Q dy (restart from it if needed; R-1)      1e-8   */
+  double pcg_rel_tol;     /* PCG acceptance: TRUE residual ||w - Q dy||_2 <= pcg_rel_tol *
+                             ||w||_2 (C-9, G15).  Inside the IPM the recursion aims at the
+                             forcing term min(pcg_rel_tol, 1e-2 mu) (>= 1e-14, at most 50
+                             iterations past acceptance), then the true residual is
+                             checked and refined by restarts (R-1)           1e-8   */
   double pcg_fallback_tol;/* relative true-residual target of the Jacobi-CG fallback run
                              (R-2)                                          1e-8   */
   double tau_viol;        /* cut violated iff lhs < 1 - tau_viol (C-3)                  1e-6   */
