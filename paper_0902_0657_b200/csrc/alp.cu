@@ -402,6 +402,8 @@ __global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layo
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   Frame F;
   frame_bind(F, &sC, &sL, slots + gw * L.slot_bytes, smem + G.bytes + warp * L.smem_bytes, lane);
+  __shared__ long long s_cyc[4][8];   // phase clocks in shared memory (a global RMW per tick
+  F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
   while (true) {
     long long f = 0;
     if (lane == 0) f = atomicAdd(counter, 1);
