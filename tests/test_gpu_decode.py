@@ -80,6 +80,13 @@ def assert_certified(code, llr, g, min_clean=1.0):
     ok = clean(g)
     assert ok.mean() >= min_clean, (ok.mean(), np.unique(g["status"], return_counts=True))
     sel = np.nonzero(ok)[0]
+    # invariants at any size on the clean frames: Thm 2a (u in [0,1]), Cor. 4 (G3: the LP output
+    # differs from the hard decision in at most m coordinates), Cor. 5 (at most m fractional entries)
+    u = g["u"][sel]
+    assert np.all(u >= -1.001e-6) and np.all(u <= 1 + 1.001e-6)
+    hd = (llr[sel] < 0).astype(np.uint8)
+    assert np.all((np.abs(u - hd) > 1e-3).sum(axis=1) <= code.m)
+    assert np.all(((u > 1e-3) & (u < 1 - 1e-3)).sum(axis=1) <= code.m)
     cert = dual_certificate_batch(code, llr[sel], g["u"][sel], g["y"][sel], g["masks"][sel])
     badm = ~cert["ok"]
     bad = sel[badm]
@@ -197,3 +204,14 @@ def test_config1_plain_cg_decode():
     g = gpu_decode(code, fb.llr, precond=1)
     assert_certified(code, fb.llr, g)
     compare(code, fb.llr, g, range(8))
+
+
+def test_large_code_fails_loudly():
+    """Config 4 (n = 32,000): the per-frame shared window exceeds the device limit; the library
+    must refuse (ALP_ERR_UNSUPPORTED), never fall back."""
+    alp = _alp()
+    from synth.codes import regular_code
+    code = regular_code(32000, 3, 6, seed=1004)
+    c = alp.Code.from_synth(code)
+    with pytest.raises(alp.AlpError):
+        alp.decode(c, torch.zeros((2, code.n), dtype=torch.float64, device="cuda"))
