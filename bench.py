@@ -341,6 +341,7 @@ def run_ours(args):
                      "kernel": "alp_decode_kernel",
                      "bytes": "sum over executed PCG iterations of B_min(p,n_act,m) (DESIGN.md §6)",
                      "peak_kind": peak_kind},
+        "pcg_phase": pcg_phase(st, pcg_bytes, t_rank / args.steps),
         "pcg": {"iters_per_s": counters[5] / (t_max / args.steps),
                 "iters_total_per_step": int(counters[5]),
                 "gbs_all_ranks": pcg_bytes_all / (t_max / args.steps) / 1e9},
@@ -385,6 +386,20 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def pcg_phase(st, pcg_bytes, t_launch):
+    """Share of the decode kernel's warp-cycles spent in the PCG loop (SpMV, sweeps, vector
+    updates; alp_frame_stats.cyc_*) and the algorithmic PCG bytes per second of PCG-phase time
+    (the kernel time scaled by that share)."""
+    keys = ("cyc_cut", "cyc_ipm", "cyc_build", "cyc_spmv", "cyc_sweep", "cyc_pcg_other")
+    tot = {k: float(st[k].sum()) for k in keys}
+    allc = sum(tot.values())
+    pcgc = tot["cyc_spmv"] + tot["cyc_sweep"] + tot["cyc_pcg_other"]
+    share = pcgc / allc if allc > 0 else 0.0
+    return {"share_of_warp_cycles": share,
+            "shares": {k: v / allc for k, v in tot.items()} if allc > 0 else {},
+            "algorithmic_gbs_in_pcg_phase": pcg_bytes / (t_launch * share) / 1e9 if share > 0 else None}
 
 
 def time_step_solve(args, dev, stream):
