@@ -563,7 +563,6 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.g_sgnC = g(2 * m);
   L.g_mask = g(2 * m);
   L.g_hist = g(8 * 256);
-  L.g_prc = g(2 * Q);
   L.g_sgnV = g(n);
   L.g_flip = g(n);
   L.slot_bytes = (long long)al(o, 256);

@@ -5,7 +5,9 @@
 // __syncwarp barriers.  Per-frame vectors live in a per-warp "slot" of global memory
 // (frame-major, contiguous, reused frame after frame so the live set stays L2-resident);
 // the latency-critical sequential parts (column sort, Alg. 7 peel, level build) and the
-// gathered PCG vectors live in the warp's shared-memory window, whose phases alias.
+// gathered PCG vectors live in the warp's shared-memory window, whose phases alias, followed
+// by whichever PCG-hot slot arrays fit the window budget (Layout::smask).  Each CTA stages the
+// Tanner graph and the code / layout descriptors in shared memory (stage_graph).
 // Citations: PAPER.md line numbers (P:n) with section / algorithm / equation label.
 #pragma once
 #include <cstdint>
@@ -79,7 +81,7 @@ __device__ __forceinline__ void stage_graph(const DCode& C, const GraphSmem& G, 
 struct Layout {
   long long slot_bytes;
   long long g_cyc, g_x, g_z, g_d2, g_v, g_y, g_dy, g_dyb, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
-      g_offF, g_sgnC, g_mask, g_hist, g_prc, g_sgnV, g_flip;
+      g_offF, g_sgnC, g_mask, g_hist, g_sgnV, g_flip;
   int smem_bytes;
   // Hot per-frame arrays that live in the warp's shared window instead of the slot
   // (bit k of smask set <=> array k at shared offset soff[k]); order = placement priority.
@@ -140,7 +142,6 @@ struct Frame {
   uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
   uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
   unsigned long long* hist;  // [alp_max_iter + 1] pool hashes of the LPs solved (C-12)
-  uint16_t* prc;   // [q]: pivot row of each column of the MTS set, NONE16 if not a pivot
   uint8_t* sgnV;   // [n]: bit k <-> k-th check of the variable present; bit 4+k <-> coef -1
   uint8_t* flip;   // [n]: 1 <-> gamma_i < 0 (x_i = 1 - u_i, §IV-B)
   long long* cyc;  // [8] per-phase clock64 accumulators (lane 0 writes; alp_frame_stats)
@@ -180,7 +181,6 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.offF = (int*)(slot + L->g_offF);
   F.sgnC = (uint16_t*)(slot + L->g_sgnC);
   F.mask = (uint16_t*)(slot + L->g_mask);
-  F.prc = (uint16_t*)(slot + L->g_prc);
   F.hist = (unsigned long long*)(slot + L->g_hist);
   F.recB = (int*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
   F.recF = (int*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
@@ -671,7 +671,6 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
     poc[pcol[R]] = (uint16_t)R;
   }
   __syncwarp();
-  for (int c = F.lane; c < C.Q; c += 32) F.prc[c] = poc[c];
   uint16_t* lvB = F.S<uint16_t>(L.s_lvB);
   uint16_t* lvF = F.S<uint16_t>(L.s_lvF);
   nLb = compute_levels<false>(F, p, lvB);
