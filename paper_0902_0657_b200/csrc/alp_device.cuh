@@ -366,7 +366,7 @@ __device__ ALP_HEAVY void sort_columns(const Frame& F) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int t = t0 + 32 * u;
-          lo[u] = 2 * j * (t / j) + (t % j);
+          lo[u] = ((t & ~(j - 1)) << 1) | (t & (j - 1));   // 2 j (t / j) + t % j, j = 2^k
           hi[u] = lo[u] + j;
           const bool ok = t < (N >> 1);
           a[u] = ok ? keys[lo[u]] : 0ull;
@@ -385,10 +385,17 @@ __device__ ALP_HEAVY void sort_columns(const Frame& F) {
       __syncwarp();
     }
   }
+  // Equal float keys are ordered by column; that is the exact (fp64 weight desc, column asc)
+  // order unless some adjacent pair inside a float tie has a strictly smaller exact weight
+  // first.  Checked in parallel; only then does the serial fix-up below run (e.g. never at
+  // IPM iteration 0, where every weight is exactly 1).
   bool tie = false;
-  for (int r = F.lane; r + 1 < C.Q; r += 32) {
+  for (int r = F.lane; r + 1 < nv; r += 32) {
     uint64_t a = keys[r], b = keys[r + 1];
-    if (a != ~0ull && b != ~0ull && (a >> 32) == (b >> 32)) tie = true;
+    if ((a >> 32) == (b >> 32)) {
+      const double wa = F.d2[(int)(a & 0xffffffffu)], wb = F.d2[(int)(b & 0xffffffffu)];
+      if (wa < wb) tie = true;
+    }
   }
   if (__any_sync(FULL, tie)) {
     if (F.lane == 0) {
