@@ -124,10 +124,11 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     for (int c = lane; c < Q; c += 32) {
       if (c >= n && !(SC[c - n] & PRESENT)) continue;
       double xc = X[c], zc = Z[c];
-      double d2 = xc / zc;
+      const double iz = 1.0 / zc;   // one division for D^2 = X Z^-1 and Z^-1 r_e
+      double d2 = xc * iz;
       double re = mu - xc * zc;
       D2[c] = d2;
-      V[c] = d2 * V[c] - re / zc;
+      V[c] = d2 * V[c] - re * iz;
     }
     __syncwarp();
 #pragma unroll 4
