@@ -73,7 +73,9 @@ def workload_config(args, ws):
     return {
         "workload": f"C2: random (3,6)-regular LDPC n=1000 m=500, {args.frames} random-codeword "
                     f"frames per GPU, BPSK/AWGN Eb/N0={SNRS[args.snr_idx]} dB, fp64 LLR, MALP-A + "
-                    "primal-dual IPM + PCG (column-wise MTS preconditioner) to rel. residual 1e-8",
+                    "primal-dual IPM + PCG (column-wise MTS preconditioner) to recursive rel. "
+                    "residual 1e-8 (forcing term min(1e-8, 1e-2 mu)) with the basis-corrected "
+                    "Newton recovery (DESIGN.md C-32)",
         "code": "rnd(3,6) n=1000 m=500 seed 1002",
         "frames_per_gpu": args.frames,
         "global_frames": args.frames * ws,
@@ -233,7 +235,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_0902_0657_b200 as alp
-    from paper_0902_0657_b200.dist import shard_frame_ids, frame_counters, reduce_run
+    from paper_0902_0657_b200.dist import shard_frame_ids, frame_counters, reduce_run, counters_dict
     from synth import config_code, config_frames
 
     code = config_code(2)
@@ -345,9 +347,7 @@ def run_ours(args):
         "pcg": {"iters_per_s": counters[5] / (t_max / args.steps),
                 "iters_total_per_step": int(counters[5]),
                 "gbs_all_ranks": pcg_bytes_all / (t_max / args.steps) / 1e9},
-        "decode": {"frames": int(counters[0]), "frame_errors": int(counters[1]),
-                   "not_certified": int(counters[2]), "lp_solves": int(counters[3]),
-                   "ipm_iters": int(counters[4]), "status_nonzero": int(counters[6])},
+        "decode": counters_dict(counters),
         "step_ms": ms,
     }
     if not args.no_e2e:
@@ -369,11 +369,8 @@ def run_ours(args):
             torch.cuda.synchronize(dev)
             cs = frame_counters(out.hard.cpu().numpy(), fbs.codewords, out.certificate.cpu().numpy(),
                                 out.status.cpu().numpy(), out.stats_numpy())
-            stv = out.status.cpu().numpy()
-            line["snr_sweep"][f"{SNRS[si]} dB"] = {
-                "frames_per_s": F / (a.elapsed_time(b) / 1e3), "frame_errors": int(cs[1]),
-                "not_certified": int(cs[2]),
-                "frames_with_cap_status": int(((stv & ~96) != 0).sum())}
+            line["snr_sweep"][f"{SNRS[si]} dB"] = dict(frames_per_s=F / (a.elapsed_time(b) / 1e3),
+                                                      **counters_dict(cs))
     if args.step_systems > 0:
         line["step_solve"] = time_step_solve(args, dev, stream)
     if ws == 1 and not args.no_cpu_baseline:
@@ -436,15 +433,39 @@ def time_step_solve(args, dev, stream):
     peak, kind = measured_peak_hbm()
     gbs = its * bmin / t / 1e9
     return {"workload": f"C5: {S} systems A D^2 A^T dy = r, (3,6) n=2000 m=1000, d = 10^U(-6,6), "
-                        "column-wise MTS PCG to true rel. residual 1e-8",
+                        "column-wise MTS PCG to recursive rel. residual 1e-8, then refined until the "
+                        "TRUE residual meets 1e-8 or the fp64 evaluation floor (PCG_FLOOR)",
             "systems_per_s": S / t, "ms_per_call": 1e3 * t, "pcg_iters_per_s": its / t,
             "mean_pcg_iters": its / S, "status_counts": {int(k): int(v) for k, v in zip(*np.unique(st, return_counts=True))},
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                          "bytes": "PCG iterations x B_min(1000, 2000, 1000) = 79 KB", "peak_kind": kind}}
 
 
+def maybe_launch_ranks(args):
+    """`--gpus N` (N > 1) without a torch.distributed environment: launch the N ranks here
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1) and return their exit
+    code; under torchrun check that WORLD_SIZE matches --gpus."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None:
+        if args.gpus > 1 and int(ws_env) != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws_env}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    rc = maybe_launch_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

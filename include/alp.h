@@ -71,33 +71,40 @@ typedef enum {
                                     pool repeated that of an LP already solved (a
                                     deterministic MALP cycle; C-12)                        */
   ALP_FRAME_IPM_MAXITER = 2,     /* some LP hit ipm_max_iter Newton steps                   */
-  ALP_FRAME_PCG_MAXITER = 4,     /* some PCG solve ended above pcg_rel_tol at pcg_max_iter  */
-  ALP_FRAME_PCG_BREAKDOWN = 8,   /* some PCG solve met h^T Q h <= 0 (or non-finite)          */
+  ALP_FRAME_PCG_MAXITER = 4,     /* some PCG recursion ended with ||r|| > pcg_rel_tol ||w||:
+                                    at pcg_max_iter, or stalled (no new residual minimum in
+                                    200 iterations; R-1).  The Newton step still
+                                    proceeds with that dy (reading C-32)                   */
+  ALP_FRAME_PCG_BREAKDOWN = 8,   /* some PCG solve met h^T Q h or z^T r = 0 / non-finite      */
   ALP_FRAME_NUMERIC = 16,        /* non-finite IPM iterate; decoding of the frame stopped   */
-  ALP_FRAME_PCG_FLOOR = 32,      /* informational: some PCG solve stopped with its TRUE
-                                    residual above pcg_rel_tol ||w|| at the fp64 attainable
-                                    accuracy: at most the evaluation floor f = 16 eps
-                                    || |A| D^2 |A|^T |dy| ||_2, or within 1e3 f with restarts
-                                    (iterative refinement) no longer halving it          */
-  ALP_FRAME_PCG_FALLBACK = 64    /* informational: some MTS-preconditioned PCG run broke down
-                                    or failed the true-residual test, and the solve was redone
-                                    by Jacobi-preconditioned CG; the better result was kept
-                                    (R-2)                                         */
+  ALP_FRAME_PCG_FLOOR = 32       /* informational, ipm_step_pcg only: the solve stopped with
+                                    its TRUE residual above pcg_rel_tol ||w|| at the fp64
+                                    attainable accuracy: at most the evaluation floor
+                                    f = 16 eps || |A| D^2 |A|^T |dy| ||_2, or within 1e3 f with
+                                    restarts (iterative refinement) no longer halving it    */
 } alp_frame_status;
 
 typedef struct alp_code alp_code;   /* opaque, immutable after creation */
 
-/* Per-frame counters (alp_decode) — 96 bytes.  cyc_* are SM clock cycles (clock64) the
+/* Per-frame counters (alp_decode) — 128 bytes.  cyc_* are SM clock cycles (clock64) the
  * frame's warp spent per phase: cut search + sign tables, IPM body (residuals, rhs,
  * Newton recovery, update), preconditioner build (sort, Alg. 7 peel, level schedule),
  * PCG SpMV, PCG preconditioner sweeps, remaining PCG work (axpys, dots, true residual). */
 typedef struct {
   int32_t lp_solves;   /* LPs solved (MALP outer iterations that added a cut)            */
   int32_t ipm_iters;   /* Newton steps summed over all LPs                                */
-  int32_t pcg_iters;   /* PCG iterations summed over all Newton steps                     */
+  int32_t pcg_iters;   /* PCG iterations summed over all Newton steps (all runs)          */
   int32_t max_p;       /* largest number of LP rows p (<= m, Cor. 3 P:289-292)             */
+  int32_t pcg_solves;  /* Newton-step solves (one per Newton step)                         */
+  int32_t pcg_p4_fail; /* solves whose final recursive residual ||r||/||w|| > pcg_rel_tol
+                          (the failure count, 0 on a fully converged frame)     */
+  int32_t pcg_true_fail; /* solves whose TRUE residual ||w - Q dy||/||w|| > pcg_rel_tol
+                          (reported, not gated: the recovery tolerates it, C-32)         */
+  int32_t reserved;
   double g_max;        /* max_i min(u_i, 1 - u_i) of the output (integrality, C-11)       */
   double pcg_bytes;    /* sum over PCG iterations of B_min(p, n_act, m)    */
+  double max_rec_relres;  /* max over the frame's solves of the recursive ||r||/||w|| at exit */
+  double max_true_relres; /* max over the frame's solves of the TRUE ||w - Q dy||/||w||     */
   int64_t cyc_cut, cyc_ipm, cyc_build, cyc_spmv, cyc_sweep, cyc_pcg_other;
   int64_t cyc_sort, cyc_peel;   /* parts of cyc_build: column sort, Alg. 7 peel */
 } alp_frame_stats;
@@ -109,13 +116,12 @@ typedef struct {
   double eta;             /* step damping of the ratio test (C-6)                0.99   */
   double gap_tol;         /* stop: x^T z <= gap_tol * (1 + |c^T x|) (C-8)               1e-9   */
   double feas_tol;        /* stop: ||r_b||, ||r_c|| <= feas_tol * (1 + ||b||, ||c||)    1e-8   */
-  double pcg_rel_tol;     /* PCG acceptance: TRUE residual ||w - Q dy||_2 <= pcg_rel_tol *
-                             ||w||_2 (C-9, G15).  Inside the IPM the recursion aims at the
-                             forcing term min(pcg_rel_tol, 1e-2 mu) (>= 1e-14, at most 50
-                             iterations past acceptance), then the true residual is
-                             checked and refined by restarts (R-1)           1e-8   */
-  double pcg_fallback_tol;/* relative true-residual target of the Jacobi-CG fallback run
-                             (R-2)                                          1e-8   */
+  double pcg_rel_tol;     /* PCG acceptance (C-9, G15): the recursive residual
+                             ||r||_2 <= pcg_rel_tol ||w||_2 at exit.  Inside the IPM the
+                             recursion aims at the forcing term min(pcg_rel_tol, 1e-2 mu)
+                             (>= 1e-14, at most 50 iterations past acceptance; DESIGN.md
+                             R-1).  ipm_step_pcg additionally refines until the TRUE
+                             residual meets it or reaches the fp64 floor          1e-8   */
   double tau_viol;        /* cut violated iff lhs < 1 - tau_viol (C-3)                  1e-6   */
   double tau_act;         /* cut active iff slack <= tau_act (C-4)                      1e-6   */
   double tau_cert;        /* certificate needs g_max <= tau_cert (C-11)                 1e-2   */
@@ -126,10 +132,11 @@ typedef struct {
   int32_t smem_frames_per_sm; /* tuning: resident frames per SM the shared-memory budget is split
                              over; hot PCG arrays move into shared memory while they fit;
                              0 = automatic (11: measured best; a small window keeps L1 large) */
-  int32_t pcg_fallback;   /* 1: MTS-PCG failures are redone by Jacobi CG (R-2); 0: report them
-                             as they are (diagnostics, e.g. residual traces)              1      */
   int32_t stop_on_lp_failure; /* 1: a frame stops decoding after an LP whose IPM hit
                              ipm_max_iter (reading C-30; status bit set, last u output)  1      */
+  int32_t basis_correction; /* 1: after each Newton step the primal residual rho = r_b - A dx
+                             left by an inexact PCG dy is removed on the preconditioner's
+                             basis columns (A_M f = rho, dx_M += f; reading C-32)        1      */
 } alp_params;
 
 /* Fills the defaults listed above (identical to the oracle's constants). */
@@ -210,6 +217,9 @@ int32_t alp_last_launch_count(void);
 
 const char* alp_status_string(alp_status s);
 const char* alp_last_error(void);
+/* Thread-local status of the last failing library call (the reason a *_workspace_bytes query
+ * returned 0, e.g. ALP_ERR_UNSUPPORTED); ALP_OK after a successful sizing query. */
+alp_status alp_last_status(void);
 const char* alp_build_info(void);
 
 #ifdef __cplusplus

@@ -35,7 +35,7 @@ DEFAULT_PARAMS = dict(
     pcg_rel_tol=1e-8,
     tau_viol=1e-6, tau_act=1e-6, tau_cert=1e-2,
     alp_max_iter=200, ipm_max_iter=100, pcg_max_iter=1000,
-    stop_on_lp_failure=1, pcg_fallback=1,
+    stop_on_lp_failure=1,
 )
 
 # per-frame status bits (mirrors include/alp.h alp_frame_status)
@@ -173,9 +173,16 @@ def step_solve_exact(A, d2: np.ndarray, w: np.ndarray, refine: int = 4) -> np.nd
     because its own forward error reaches kappa * eps."""
     A = np.asarray(A.todense()) if sp.issparse(A) else np.asarray(A)
     ld = np.longdouble
-    Al = A.astype(ld)
-    Q = (Al * np.asarray(d2, dtype=np.float64).astype(ld)) @ Al.T
-    p = Q.shape[0]
+    p = A.shape[0]
+    # Q = sum_i d2_i a_i a_i^T over the columns a_i of A (the definition, summed column by
+    # column; A is +-1/0 so each term is exact in longdouble) — only the nonzeros of a_i touch Q
+    Q = np.zeros((p, p), dtype=ld)
+    d2l = np.asarray(d2, dtype=np.float64).astype(ld)
+    for i in range(A.shape[1]):
+        nz = np.nonzero(A[:, i])[0]
+        if nz.size:
+            a = A[nz, i].astype(ld)
+            Q[np.ix_(nz, nz)] += d2l[i] * np.outer(a, a)
     if p == 0:
         return np.zeros(0)
     L = np.zeros_like(Q)
@@ -308,15 +315,17 @@ def slack_of(code, j: int, inV, u: np.ndarray) -> float:
     return cut_lhs(u[code.N(j)], inV) - 1.0
 
 
-def decode_outputs(code, gamma, u, tau_cert):
+def decode_outputs(code, gamma, u, tau_cert, lp_converged=True):
     """Hard decision [u_i > 1/2] (C-14), objective gamma^T u (C-13), g_max and the
-    ML certificate: integral (g_max <= tau_cert, C-11) and H hard = 0 mod 2."""
+    ML certificate: integral (g_max <= tau_cert, C-11) and H hard = 0 mod 2.
+    The certificate claims u is the LP optimum; when the last LP's IPM did not converge
+    (Newton-step cap or non-finite iterate) u is not, and it never certifies (C-31)."""
     gamma = np.asarray(gamma, dtype=np.float64)
     hard = (u > 0.5).astype(np.uint8)
     obj = float(gamma @ u)
     g_max = float(np.max(np.minimum(u, 1.0 - u))) if u.size else 0.0
     parity_ok = all(int(hard[code.N(j)].sum()) % 2 == 0 for j in range(code.m))
-    cert = int(g_max <= tau_cert and parity_ok)
+    cert = int(g_max <= tau_cert and parity_ok and lp_converged)
     return hard, obj, g_max, cert
 
 
@@ -346,6 +355,7 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
     trace = []
     objs = []
     seen_pools = set()      # reading C-12: a repeated pool is a deterministic cycle
+    last_lp_ok = True       # the last solved LP converged (C-31)
     for k in range(P["alp_max_iter"] + 1):
         changed = False
         if variant == "B":
@@ -387,6 +397,7 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
         chol_fixes += res["chol_fixes"]
         pcg_iters += res["pcg_iters"]
         status |= res["status"] & (ST_IPM_MAXITER | ST_NUMERIC | ST_PCG_MAXITER | ST_PCG_BREAKDOWN)
+        last_lp_ok = not (res["status"] & (ST_IPM_MAXITER | ST_NUMERIC))
         xs = res["x"][:n]
         u = np.where(lp["flip"], 1.0 - xs, xs)
         y_check = np.zeros(m)
@@ -402,7 +413,7 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
             # reading C-30: an LP that did not converge gives no trustworthy u for the next
             # cut search; the frame stops with its status bits and the last u
             break
-    hard, obj, g_max, cert = decode_outputs(code, gamma, u, P["tau_cert"])
+    hard, obj, g_max, cert = decode_outputs(code, gamma, u, P["tau_cert"], last_lp_ok)
     masks = np.zeros(m, dtype=np.uint16)
     if variant != "ALP":
         for j, inV in pool.items():

@@ -13,31 +13,37 @@ class AlpParams(C.Structure):
         ("variant", C.c_int32), ("precond", C.c_int32),
         ("sigma", C.c_double), ("eta", C.c_double),
         ("gap_tol", C.c_double), ("feas_tol", C.c_double), ("pcg_rel_tol", C.c_double),
-        ("pcg_fallback_tol", C.c_double),
         ("tau_viol", C.c_double), ("tau_act", C.c_double), ("tau_cert", C.c_double),
         ("alp_max_iter", C.c_int32), ("ipm_max_iter", C.c_int32), ("pcg_max_iter", C.c_int32),
         ("warps_per_block", C.c_int32), ("smem_frames_per_sm", C.c_int32),
-        ("pcg_fallback", C.c_int32), ("stop_on_lp_failure", C.c_int32),
+        ("stop_on_lp_failure", C.c_int32),
+        ("basis_correction", C.c_int32),
     ]
 
 
 class FrameStats(C.Structure):
     _fields_ = [
         ("lp_solves", C.c_int32), ("ipm_iters", C.c_int32), ("pcg_iters", C.c_int32),
-        ("max_p", C.c_int32), ("g_max", C.c_double), ("pcg_bytes", C.c_double),
+        ("max_p", C.c_int32), ("pcg_solves", C.c_int32), ("pcg_p4_fail", C.c_int32),
+        ("pcg_true_fail", C.c_int32), ("reserved", C.c_int32),
+        ("g_max", C.c_double), ("pcg_bytes", C.c_double),
+        ("max_rec_relres", C.c_double), ("max_true_relres", C.c_double),
         ("cyc_cut", C.c_int64), ("cyc_ipm", C.c_int64), ("cyc_build", C.c_int64),
         ("cyc_spmv", C.c_int64), ("cyc_sweep", C.c_int64), ("cyc_pcg_other", C.c_int64),
         ("cyc_sort", C.c_int64), ("cyc_peel", C.c_int64),
     ]
 
 
-# numpy dtype of alp_frame_stats (80 bytes) for zero-copy views of device/host buffers
+# numpy dtype of alp_frame_stats (128 bytes) for zero-copy views of device/host buffers
 STATS_FIELDS = [("lp_solves", "<i4"), ("ipm_iters", "<i4"), ("pcg_iters", "<i4"),
-                ("max_p", "<i4"), ("g_max", "<f8"), ("pcg_bytes", "<f8"),
+                ("max_p", "<i4"), ("pcg_solves", "<i4"), ("pcg_p4_fail", "<i4"),
+                ("pcg_true_fail", "<i4"), ("reserved", "<i4"),
+                ("g_max", "<f8"), ("pcg_bytes", "<f8"),
+                ("max_rec_relres", "<f8"), ("max_true_relres", "<f8"),
                 ("cyc_cut", "<i8"), ("cyc_ipm", "<i8"), ("cyc_build", "<i8"),
                 ("cyc_spmv", "<i8"), ("cyc_sweep", "<i8"), ("cyc_pcg_other", "<i8"),
                 ("cyc_sort", "<i8"), ("cyc_peel", "<i8")]
-STATS_BYTES = 96
+STATS_BYTES = 128
 
 P = C.c_void_p
 SIGNATURES = {
@@ -57,6 +63,7 @@ SIGNATURES = {
     "alp_debug_trace": (C.c_int, [P, C.c_int32]),
     "alp_status_string": (C.c_char_p, [C.c_int]),
     "alp_last_error": (C.c_char_p, []),
+    "alp_last_status": (C.c_int, []),
     "alp_build_info": (C.c_char_p, []),
 }
 

@@ -18,7 +18,7 @@ from ._ffi import AlpParams, STATS_FIELDS, STATS_BYTES
 STATUS_NAMES = {0: "ALP_OK", -1: "ALP_ERR_INVALID_ARG", -2: "ALP_ERR_BAD_CODE",
                 -3: "ALP_ERR_UNSUPPORTED", -4: "ALP_ERR_CUDA", -5: "ALP_ERR_WORKSPACE"}
 FRAME_ALP_MAXITER, FRAME_IPM_MAXITER, FRAME_PCG_MAXITER, FRAME_PCG_BREAKDOWN, FRAME_NUMERIC = 1, 2, 4, 8, 16
-FRAME_PCG_FLOOR, FRAME_PCG_FALLBACK = 32, 64   # informational (include/alp.h)
+FRAME_PCG_FLOOR = 32   # informational (include/alp.h; ipm_step_pcg only)
 STATS_DTYPE = np.dtype(STATS_FIELDS)
 
 
@@ -45,6 +45,13 @@ def default_params(**kw) -> AlpParams:
             raise KeyError(k)
         setattr(p, k, v)
     return p
+
+
+def _sizing_error() -> AlpError:
+    """Error of a *_workspace_bytes query that returned 0: the library's own failing status
+    (e.g. ALP_ERR_UNSUPPORTED), never a generic one."""
+    st = int(lib().alp_last_status())
+    return AlpError(st if st != 0 else -1, lib().alp_last_error().decode())
 
 
 def _ptr(t) -> int | None:
@@ -114,7 +121,7 @@ class DecodeResult:
     objective: torch.Tensor   # [F] float64
     certificate: torch.Tensor  # [F] uint8
     status: torch.Tensor      # [F] int32
-    stats: torch.Tensor       # [F, 96] uint8 (alp_frame_stats); see stats_numpy()
+    stats: torch.Tensor       # [F, 128] uint8 (alp_frame_stats); see stats_numpy()
     u: torch.Tensor | None = None
     y: torch.Tensor | None = None
     masks: torch.Tensor | None = None
@@ -146,7 +153,7 @@ def decode(code: Code, llr: torch.Tensor, params: AlpParams | None = None, want_
     pp = C.byref(params) if params is not None else None
     nbytes = lib().alp_decode_workspace_bytes(code.handle, F, pp)
     if nbytes == 0 and F > 0:
-        raise AlpError(-1, lib().alp_last_error().decode())
+        raise _sizing_error()
     ws = (workspace or _ws("decode", dev)).get(nbytes)
     _check(lib().alp_decode(code.handle, F, _ptr(llr), _ptr(out.hard), _ptr(out.objective),
                             _ptr(out.certificate), _ptr(out.status), _ptr(out.stats), _ptr(out.u),
@@ -171,7 +178,7 @@ def decode_host(code: Code, llr_host: torch.Tensor, params: AlpParams | None = N
     pp = C.byref(params) if params is not None else None
     nbytes = lib().alp_decode_host_workspace_bytes(code.handle, F, pp)
     if nbytes == 0 and F > 0:
-        raise AlpError(-1, lib().alp_last_error().decode())
+        raise _sizing_error()
     ws = (workspace or _ws("decode_host", "cuda")).get(nbytes)
     _check(lib().alp_decode_host(code.handle, F, _ptr(llr_host), _ptr(out["hard"]),
                                  _ptr(out["objective"]), _ptr(out["certificate"]), _ptr(out["status"]),
@@ -217,7 +224,7 @@ def ipm_step_pcg(code: Code, masks: torch.Tensor, d: torch.Tensor, r: torch.Tens
     pp = C.byref(params) if params is not None else None
     nbytes = lib().alp_pcg_workspace_bytes(code.handle, S, pp)
     if nbytes == 0 and S > 0:
-        raise AlpError(-1, lib().alp_last_error().decode())
+        raise _sizing_error()
     ws = (workspace or _ws("pcg", dev)).get(nbytes)
     _check(lib().ipm_step_pcg(code.handle, S, _ptr(masks), _ptr(flip), _ptr(d), _ptr(r), _ptr(res.dy),
                               _ptr(res.iters), _ptr(res.relres), _ptr(res.status), _ptr(res.pivot_rows),

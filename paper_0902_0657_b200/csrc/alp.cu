@@ -5,6 +5,7 @@
 // runs the whole adaptive-LP decode of that frame (Alg. 3 with the IPM of §IV-B and the
 // PCG of Alg. 4 preconditioned by Alg. 7) and writes its outputs; no host round trips.
 #include <algorithm>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -25,8 +26,8 @@ __device__ int g_trace_cap = 0;
 __device__ int g_trace_n = 0;
 
 struct IpmOut {
-  int iters, status, pcg_iters;
-  double pcg_bytes;
+  int iters, status, pcg_iters, solves, p4_fail, true_fail;
+  double pcg_bytes, max_rec, max_true;
 };
 
 // =====================================================================================
@@ -58,6 +59,8 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
   const double* DY = F.dy;
   const uint16_t* __restrict__ SC = F.sgnC;
   const uint8_t* __restrict__ SV = F.sgnV;
+  double* __restrict__ RBv = F.rb;   // r_b and r_c of the current iterate (kept for the recovery)
+  double* __restrict__ RCv = F.rc;
   const double s0 = fmax(1.0, fmax(bmax, cmax));
   for (int c = lane; c < Q; c += 32) {
     bool valid = (c < n) || (SC[c - n] & PRESENT);
@@ -66,11 +69,11 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
   }
   for (int j = lane; j < m; j += 32) Y[j] = 0.0;
   __syncwarp();
-  IpmOut out{0, 0, 0, 0.0};
+  IpmOut out{0, 0, 0, 0, 0, 0, 0.0, 0.0, 0.0};
   long long tk = clock64();
   // algorithmic bytes per PCG iteration of this LP
   const double Bmin = 8.0 * (nact + p) + 48.0 * p + 5.0 * p + 2.0 * m;
-  int it = 0, bad_solves = 0;
+  int it = 0;
   while (true) {
     double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
 #pragma unroll 4
@@ -84,9 +87,11 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
         acc = ((s >> t) & 1) ? acc + xi : acc - xi;
       }
       W[j] = acc;
+      RBv[j] = acc;
       rbn = fmax(rbn, fabs(acc));
       double rc = -Y[j] - Z[n + j];
       V[n + j] = rc;
+      RCv[n + j] = rc;
       rcn = fmax(rcn, fabs(rc));
       gap += X[n + j] * Z[n + j];
     }
@@ -102,6 +107,7 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
         acc = ((s >> (4 + k)) & 1) ? acc + yj : acc - yj;
       }
       V[i] = acc;
+      RCv[i] = acc;
       rcn = fmax(rcn, fabs(acc));
       double xi = X[i];
       gap += xi * Z[i];
@@ -147,26 +153,24 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     int nLb = 0, nLf = 0;
     const bool mtm = (P.precond == 0);
     ALP_TICK(F, CY_IPM, tk);
-    if (mtm) build_precond(F, p, nLb, nLf);
+    // the Alg. 7 triangular set is both the PCG preconditioner (precond = 0) and the basis of
+    // the step's feasibility correction (C-32), so plain CG builds it too when that is on
+    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf);
     ALP_TICK(F, CY_BUILD, tk);
-    // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to
-    // well below z ~ mu on the basic columns, so late in the IPM the recursion runs to
-    // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); acceptance stays ||w - Q dy|| <= 1e-8||w||
+    // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to well
+    // below z ~ mu on the basic columns, so late in the IPM the recursion aims at
+    // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); P4 acceptance is pcg_rel_tol.  An inexact
+    // dy is admissible because the recovery below keeps every KKT row but the complementarity
+    // of the basis columns exact (C-32).
     const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, 1e-2 * mu));
-    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, inner, 1e-6);
+    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, inner, false);
     tk = clock64();
-
     out.status |= pr.status;
-    // three consecutive step solves that failed even after the fallback: the Newton direction
-    // is garbage and the IPM cannot progress; give the LP up as non-converged (C-30)
-    bad_solves = (pr.status & (ST_PCG_MAXITER | ST_PCG_BREAKDOWN)) ? bad_solves + 1 : 0;
-    if (bad_solves >= 3) {
-      out.status |= ST_IPM_MAXITER;
-      out.pcg_iters += pr.iters;
-      out.pcg_bytes += (double)pr.iters * Bmin;
-      it++;
-      break;
-    }
+    out.solves += 1;
+    out.p4_fail += (pr.status != 0) ? 1 : 0;
+    out.true_fail += (pr.relres > P.pcg_rel_tol) ? 1 : 0;
+    out.max_rec = fmax(out.max_rec, pr.rec_relres);
+    out.max_true = fmax(out.max_true, pr.relres);
     if (g_trace) {
       double dmn = 1e308, dmx = 0.0;
       for (int c = lane; c < Q; c += 32) {
@@ -184,7 +188,13 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     }
     out.pcg_iters += pr.iters;
     out.pcg_bytes += (double)pr.iters * Bmin;
-    double ax = 1e308, az = 1e308;
+    // Newton recovery (eq.`Delta x`, eq.`Delta z` P:480-481).  dz is taken in the algebraically
+    // identical form dz = r_c - A^T dy (eliminate dx from eq.`Delta z`), which keeps the dual
+    // equation A^T(y+dy) + z + dz = c exact for ANY dy; with dx from eq.`Delta x` the
+    // complementarity row Z dx + X dz = r_e is then exact too, so an inexact PCG dy only leaves
+    // the primal row off by the step residual rho = r_b - A dx = w - Q dy.  That residual is
+    // moved onto the preconditioner's basis columns: A_M f = rho (the back sweep of P:585),
+    // dx_M += f, so A dx = r_b holds to rounding (reading C-32; R-1).
 #pragma unroll 4
     for (int i = lane; i < n; i += 32) {
       uint8_t s = SV[i];
@@ -195,28 +205,53 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
         double d = DY[var_ck(C, i, k)];
         atdy = ((s >> (4 + k)) & 1) ? atdy - d : atdy + d;
       }
-      double xc = X[i], zc = Z[i];
-      double dx = D2[i] * atdy - V[i];
-      double re = mu - xc * zc;
-      double dz = (re - zc * dx) / xc;
-      if (dx < 0.0) ax = fmin(ax, -xc / dx);
-      if (dz < 0.0) az = fmin(az, -zc / dz);
+      const double dx = D2[i] * atdy - V[i];
       V[i] = dx;
-      D2[i] = dz;
+      D2[i] = RCv[i] - atdy;   // dz
     }
     for (int j = lane; j < m; j += 32) {
       if (!(SC[j] & PRESENT)) continue;
-      int c = n + j;
-      double xc = X[c], zc = Z[c];
-      double dx = D2[c] * DY[j] - V[c];
-      double re = mu - xc * zc;
-      double dz = (re - zc * dx) / xc;
-      if (dx < 0.0) ax = fmin(ax, -xc / dx);
-      if (dz < 0.0) az = fmin(az, -zc / dz);
+      const int c = n + j;
+      const double dx = D2[c] * DY[j] - V[c];
       V[c] = dx;
-      D2[c] = dz;
+      D2[c] = RCv[c] - DY[j];
     }
     __syncwarp();
+    if (P.basis_correction && nLb > 0) {
+      double* rS = F.S<double>(F.L->s_r);
+      const double* fS = F.S<double>(F.L->s_f);
+      for (int j = lane; j < m; j += 32) {
+        uint16_t s = SC[j];
+        double rho = 0.0;
+        if (s & PRESENT) {
+          int deg = C.chk_deg[j];
+          double acc = RBv[j] - V[n + j];
+          for (int t = 0; t < deg; ++t) {
+            double xi = V[chk_nb(C, j, t)];
+            acc = ((s >> t) & 1) ? acc + xi : acc - xi;
+          }
+          rho = acc;
+        }
+        rS[j] = rho;
+      }
+      __syncwarp();
+      back_sweep(F, nLb);   // f = A_M^-1 rho, f_R = component of row R's pivot column
+      __syncwarp();
+      for (int j = lane; j < m; j += 32) {
+        const uint16_t c = F.pcolR[j];
+        if (c != NONE16) V[c] += fS[j];
+      }
+      __syncwarp();
+    }
+    // ratio test (C-6)
+    double ax = 1e308, az = 1e308;
+#pragma unroll 4
+    for (int c = lane; c < Q; c += 32) {
+      if (c >= n && !(SC[c - n] & PRESENT)) continue;
+      const double dx = V[c], dz = D2[c];
+      if (dx < 0.0) ax = fmin(ax, -X[c] / dx);
+      if (dz < 0.0) az = fmin(az, -Z[c] / dz);
+    }
     ax = wmin(ax);
     az = wmin(az);
     const double bP = fmin(1.0, P.eta * ax);
@@ -280,6 +315,9 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   const double cmax = wmax(cm);
   __syncwarp();
   int status = 0, lp_solves = 0, ipm_iters = 0, pcg_iters = 0, max_p = 0;
+  int solves = 0, p4_fail = 0, true_fail = 0;
+  double max_rec = 0.0, max_true = 0.0;
+  bool last_lp_bad = false;   // the last solved LP did not converge (IPM cap / non-finite)
   double pcg_bytes = 0.0;
   if (lane < 8) F.cyc[lane] = 0;
   __syncwarp();
@@ -323,9 +361,15 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
     max_p = max(max_p, p);
     IpmOut o = ipm_solve(F, P, g, p, nact, bmax, cmax, f, lp_solves);
     status |= o.status;
+    last_lp_bad = (o.status & (ST_IPM_MAXITER | ST_NUMERIC)) != 0;
     ipm_iters += o.iters;
     pcg_iters += o.pcg_iters;
     pcg_bytes += o.pcg_bytes;
+    solves += o.solves;
+    p4_fail += o.p4_fail;
+    true_fail += o.true_fail;
+    max_rec = fmax(max_rec, o.max_rec);
+    max_true = fmax(max_true, o.max_true);
     for (int i = lane; i < n; i += 32) {
       double xi = F.x[i];
       F.u[i] = F.flip[i] ? 1.0 - xi : xi;
@@ -362,7 +406,9 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   bool pbad = __any_sync(FULL, parity_bad);
   if (lane == 0) {
     O.objective[f] = obj;
-    O.cert[f] = (gm <= P.tau_cert && !pbad) ? 1 : 0;
+    // ML certificate (C-11): an integral codeword that is the optimum of the LP; an LP
+    // whose IPM did not converge proves nothing, so its u never certifies (C-31)
+    O.cert[f] = (gm <= P.tau_cert && !pbad && !last_lp_bad) ? 1 : 0;
     if (O.status) O.status[f] = status;
     if (O.stats) {
       alp_frame_stats st;
@@ -370,6 +416,12 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
       st.ipm_iters = ipm_iters;
       st.pcg_iters = pcg_iters;
       st.max_p = max_p;
+      st.pcg_solves = solves;
+      st.pcg_p4_fail = p4_fail;
+      st.pcg_true_fail = true_fail;
+      st.reserved = 0;
+      st.max_rec_relres = max_rec;
+      st.max_true_relres = max_true;
       st.g_max = gm;
       st.pcg_bytes = pcg_bytes;
       st.cyc_cut = F.cyc[CY_CUT];
@@ -390,7 +442,7 @@ __global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layo
                                                         char* slots,
                                                         const double* __restrict__ llr,
                                                         long long n_frames, DecodeOut O,
-                                                        int* counter) {
+                                                        unsigned long long* counter) {
   extern __shared__ __align__(16) char smem[];
   __shared__ DCode sC;    // code / layout descriptors in shared memory: the Frame's pointers to
   __shared__ Layout sL;   // them must not land in local memory
@@ -407,7 +459,7 @@ __global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layo
   F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
   while (true) {
     long long f = 0;
-    if (lane == 0) f = atomicAdd(counter, 1);
+    if (lane == 0) f = (long long)atomicAdd(counter, 1ull);   // 64-bit: no wrap at any n_frames
     f = __shfl_sync(FULL, f, 0);
     if (f >= n_frames) break;
     decode_frame(F, P, llr + f * C.n, f, O);
@@ -430,7 +482,7 @@ struct StepIO {
 // Isolated step solve (eq.`Delta y` P:479) per system: signs, D^2, Alg. 7, PCG.
 __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout L, GraphSmem G,
                                                       char* slots, long long n_sys, StepIO io,
-                                                      int* counter) {
+                                                      unsigned long long* counter) {
   extern __shared__ __align__(16) char smem[];
   __shared__ DCode sC;
   __shared__ Layout sL;
@@ -446,7 +498,7 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
   const int n = C.n, m = C.m, Q = C.Q;
   while (true) {
     long long s = 0;
-    if (lane == 0) s = atomicAdd(counter, 1);
+    if (lane == 0) s = (long long)atomicAdd(counter, 1ull);
     s = __shfl_sync(FULL, s, 0);
     if (s >= n_sys) break;
     for (int j = lane; j < m; j += 32) F.mask[j] = io.masks[s * m + j];
@@ -472,7 +524,7 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
           if (io.pcol) io.pcol[s * m + k] = -1;
         }
     }
-    PcgResult pr = pcg_solve(F, P, mtm, nLb, nLf, P.pcg_rel_tol, 1.0);
+    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, P.pcg_rel_tol, true);
     for (int j = lane; j < m; j += 32) io.dy[s * m + j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
     if (lane == 0) {
       if (io.iters) io.iters[s] = pr.iters;
@@ -501,10 +553,12 @@ struct alp_code {
 
 namespace {
 thread_local std::string g_last_error;
+thread_local alp_status g_last_status = ALP_OK;
 thread_local int g_last_launches = 0;
 
 alp_status fail(alp_status s, const std::string& msg) {
   g_last_error = msg;
+  g_last_status = s;
   return s;
 }
 alp_status cuda_fail(cudaError_t e, const char* what) {
@@ -551,7 +605,6 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.g_v = g(8 * Q);
   L.g_y = g(8 * m);
   L.g_dy = g(8 * m);
-  L.g_dyb = g(8 * m);
   L.g_l = g(8 * m);
   L.g_w = g(8 * m);
   L.g_u = g(8 * n);
@@ -566,6 +619,9 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.g_hist = g(8 * 256);
   L.g_sgnV = g(n);
   L.g_flip = g(n);
+  L.g_rb = g(8 * m);
+  L.g_rc = g(8 * Q);
+  L.g_pcol = g(2 * m);
   L.slot_bytes = (long long)al(o, 256);
   // shared window
   size_t s_sort = 8 * (size_t)C.QP2;
@@ -679,9 +735,8 @@ Params make_params(const alp_params* p) {
   P.gap_tol = p->gap_tol;
   P.feas_tol = p->feas_tol;
   P.pcg_rel_tol = p->pcg_rel_tol;
-  P.pcg_fallback_tol = p->pcg_fallback_tol;
   P.stop_on_lp_failure = p->stop_on_lp_failure;
-  P.pcg_fallback = p->pcg_fallback;
+  P.basis_correction = p->basis_correction;
   P.tau_viol = p->tau_viol;
   P.tau_act = p->tau_act;
   P.tau_cert = p->tau_cert;
@@ -702,6 +757,19 @@ alp_status check_params(const alp_params* p) {
   if (p->warps_per_block < 0 || p->warps_per_block > 4 || p->smem_frames_per_sm < 0 || p->smem_frames_per_sm > 32)
     return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..4, smem_frames_per_sm 0..32");
   return ALP_OK;
+}
+
+template <class K>
+cudaError_t raise_smem_optin(K kernel, int dev, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;   // (kernel, device) pairs already set
+  std::lock_guard<std::mutex> lk(mu);
+  const void* key = reinterpret_cast<const void*>(kernel);
+  for (auto& d : done)
+    if (d.first == key && d.second == dev) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(key, dev);
+  return e;
 }
 
 struct LaunchCfg {
@@ -726,7 +794,10 @@ alp_status plan_launch(K kernel, const Layout& L, int graph_bytes, long long uni
     return fail(ALP_ERR_UNSUPPORTED, "per-frame shared memory " + std::to_string(L.smem_bytes) +
                                          " B exceeds the device limit");
   int smem_block = wpb * L.smem_bytes + graph_bytes;
-  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_block);
+  // The dynamic shared-memory opt-in is raised once per (kernel, device) to the device maximum,
+  // never lowered per call: concurrent calls with different tuning params then cannot undo
+  // each other's attribute between set and launch (include/alp.h thread-safety note).
+  e = raise_smem_optin(kernel, dev, smem_optin);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   int nb = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, 32 * wpb, smem_block);
@@ -757,7 +828,6 @@ void alp_default_params(alp_params* p) {
   p->gap_tol = 1e-9;
   p->feas_tol = 1e-8;
   p->pcg_rel_tol = 1e-8;
-  p->pcg_fallback_tol = 1e-8;
   p->tau_viol = 1e-6;
   p->tau_act = 1e-6;
   p->tau_cert = 1e-2;
@@ -767,7 +837,7 @@ void alp_default_params(alp_params* p) {
   p->warps_per_block = 0;
   p->smem_frames_per_sm = 0;
   p->stop_on_lp_failure = 1;
-  p->pcg_fallback = 1;
+  p->basis_correction = 1;
 }
 
 const char* alp_status_string(alp_status s) {
@@ -783,6 +853,8 @@ const char* alp_status_string(alp_status s) {
 }
 
 const char* alp_last_error(void) { return g_last_error.c_str(); }
+
+alp_status alp_last_status(void) { return g_last_status; }
 
 const char* alp_build_info(void) {
   return "libalp: sm_100a, warp-per-frame persistent kernels, fp64";
@@ -886,6 +958,7 @@ alp_status alp_code_destroy(alp_code* c) {
 }
 
 size_t alp_decode_workspace_bytes(const alp_code* code, int64_t n_frames, const alp_params* params) {
+  g_last_status = ALP_OK;
   if (!code || n_frames < 0 || check_params(params) != ALP_OK) {
     if (!code || n_frames < 0) fail(ALP_ERR_INVALID_ARG, "bad code or n_frames");
     return 0;
@@ -898,6 +971,7 @@ size_t alp_decode_workspace_bytes(const alp_code* code, int64_t n_frames, const 
 }
 
 size_t alp_pcg_workspace_bytes(const alp_code* code, int64_t n_sys, const alp_params* params) {
+  g_last_status = ALP_OK;
   if (!code || n_sys < 0 || check_params(params) != ALP_OK) {
     if (!code || n_sys < 0) fail(ALP_ERR_INVALID_ARG, "bad code or n_sys");
     return 0;
@@ -934,8 +1008,8 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
   if (workspace_bytes < need)
     return fail(ALP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   cudaStream_t s = (cudaStream_t)stream;
-  int* counter = (int*)workspace;
-  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+  unsigned long long* counter = (unsigned long long*)workspace;
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(*counter), s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   DecodeOut O{hard, objective, certificate, frame_status, stats, u_out, y_out, mask_out};
   alp_decode_kernel<<<cfg.grid, 32 * cfg.wpb, cfg.smem_block, s>>>(
@@ -965,7 +1039,7 @@ alp_status alp_decode_host(const alp_code* code, int64_t n_frames, const double*
   if (!llr_host || !hard_host || !objective_host || !certificate_host)
     return fail(ALP_ERR_INVALID_ARG, "llr, hard, objective and certificate are required");
   size_t base = alp_decode_workspace_bytes(code, n_frames, params);
-  if (!base) return ALP_ERR_INVALID_ARG;
+  if (!base) return g_last_status != ALP_OK ? g_last_status : ALP_ERR_INVALID_ARG;
   size_t need = alp_decode_host_workspace_bytes(code, n_frames, params);
   if (!workspace || ((uintptr_t)workspace & 255) || workspace_bytes < need)
     return fail(ALP_ERR_WORKSPACE, "workspace NULL, misaligned or too small: need " + std::to_string(need));
@@ -1026,8 +1100,8 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   if (workspace_bytes < need)
     return fail(ALP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   cudaStream_t s = (cudaStream_t)stream;
-  int* counter = (int*)workspace;
-  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+  unsigned long long* counter = (unsigned long long*)workspace;
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(*counter), s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   StepIO io{masks, flip, d, r, dy, pcg_iters, rel_res, sys_status, pivot_rows, pivot_cols};
   pcg_step_kernel<<<cfg.grid, 32 * cfg.wpb, cfg.smem_block, s>>>(

@@ -31,13 +31,13 @@ constexpr int RF = 4;      // forward-record ints: head + up to d_v - 1 deps
 
 // frame status bits (include/alp.h alp_frame_status)
 constexpr int ST_ALP_MAXITER = 1, ST_IPM_MAXITER = 2, ST_PCG_MAXITER = 4, ST_PCG_BREAKDOWN = 8,
-              ST_NUMERIC = 16, ST_PCG_FLOOR = 32, ST_PCG_FALLBACK = 64;
+              ST_NUMERIC = 16, ST_PCG_FLOOR = 32;
 
 struct Params {
   int variant, precond;
-  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, pcg_fallback_tol, tau_viol, tau_act, tau_cert;
+  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, tau_viol, tau_act, tau_cert;
   int alp_max_iter, ipm_max_iter, pcg_max_iter;
-  int pcg_fallback, stop_on_lp_failure;
+  int stop_on_lp_failure, basis_correction;
 };
 
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
@@ -80,8 +80,8 @@ __device__ __forceinline__ void stage_graph(const DCode& C, const GraphSmem& G, 
 // Byte offsets inside one warp's global slot and shared-memory window (host-computed).
 struct Layout {
   long long slot_bytes;
-  long long g_cyc, g_x, g_z, g_d2, g_v, g_y, g_dy, g_dyb, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
-      g_offF, g_sgnC, g_mask, g_hist, g_sgnV, g_flip;
+  long long g_cyc, g_x, g_z, g_d2, g_v, g_y, g_dy, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
+      g_offF, g_sgnC, g_mask, g_hist, g_sgnV, g_flip, g_rb, g_rc, g_pcol;
   int smem_bytes;
   // Hot per-frame arrays that live in the warp's shared window instead of the slot
   // (bit k of smask set <=> array k at shared offset soff[k]); order = placement priority.
@@ -137,7 +137,8 @@ struct Frame {
   const Layout* L;
   int lane;
   char* sm;
-  double *x, *z, *d2, *v, *y, *dy, *dyb, *l, *w, *u, *b, *dinvF;
+  double *x, *z, *d2, *v, *y, *dy, *l, *w, *u, *b, *dinvF, *rb, *rc;
+  uint16_t* pcolR;  // [m]: pivot column of pivot row R (0..n+m-1), NONE16 if R is not a pivot
   int *recB, *recF, *offB, *offF;
   uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
   uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
@@ -169,7 +170,6 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.v = (double*)(slot + L->g_v);
   F.y = (double*)(slot + L->g_y);
   F.dy = (double*)(slot + L->g_dy);
-  F.dyb = (double*)(slot + L->g_dyb);
   F.l = (double*)(slot + L->g_l);
   F.w = (double*)(slot + L->g_w);
   F.u = (double*)(slot + L->g_u);
@@ -182,6 +182,9 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.sgnC = (uint16_t*)(slot + L->g_sgnC);
   F.mask = (uint16_t*)(slot + L->g_mask);
   F.hist = (unsigned long long*)(slot + L->g_hist);
+  F.rb = (double*)(slot + L->g_rb);
+  F.rc = (double*)(slot + L->g_rc);
+  F.pcolR = (uint16_t*)(slot + L->g_pcol);
   F.recB = (int*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
   F.recF = (int*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
   F.offB = (int*)rel_ptr(L, slot, sm, RL_OFFB, L->g_offB);
@@ -193,7 +196,6 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.l = (double*)rel_ptr(L, slot, sm, RL_L, L->g_l);
   F.dy = (double*)rel_ptr(L, slot, sm, RL_DY, L->g_dy);
   F.w = (double*)rel_ptr(L, slot, sm, RL_W, L->g_w);
-  F.sgnV = (uint8_t*)(slot + L->g_sgnV);
   F.flip = (uint8_t*)(slot + L->g_flip);
 }
 
@@ -672,10 +674,12 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
   const uint16_t* prow = F.S<uint16_t>(L.s_prow);
   const uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
   for (int c = F.lane; c < C.Q; c += 32) poc[c] = NONE16;
+  for (int j = F.lane; j < C.m; j += 32) F.pcolR[j] = NONE16;
   __syncwarp();
   for (int k = F.lane; k < p; k += 32) {
     int R = prow[k];
     poc[pcol[R]] = (uint16_t)R;
+    F.pcolR[R] = pcol[R];   // kept past the PCG (the peel arrays are aliased by its vectors)
   }
   __syncwarp();
   uint16_t* lvB = F.S<uint16_t>(L.s_lvB);
@@ -871,36 +875,34 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
   return rz;
 }
 
-// Preconditioner modes of one PCG attempt.
-constexpr int PC_MTS = 0, PC_NONE = 1, PC_JACOBI = 2;
+// Preconditioner modes of one PCG run.
+constexpr int PC_MTS = 0, PC_NONE = 1;
 
 __device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb, int nLf,
                                               double& rz) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
   double* rS = F.S<double>(L.s_r);
-  double* fS = F.S<double>(L.s_f);
   double* zS = F.S<double>(L.s_z);
-  double acc_rz = 0.0;
-  if (mode != PC_MTS) {   // identity (plain CG) or Jacobi z = r / diag(Q) (dinvF)
+  if (mode != PC_MTS) {   // identity (plain CG)
+    double acc_rz = 0.0;
     for (int j = F.lane; j < C.m; j += 32) {
       double r = rS[j];
-      double z = (mode == PC_JACOBI) ? r * F.dinvF[j] : r;
-      zS[j] = z;
-      acc_rz += r * z;   // sum of r_j^2 / Q_jj >= 0
+      zS[j] = r;
+      acc_rz += r * r;
     }
     __syncwarp();
     rz = wsum(acc_rz);
     return;
   }
   back_sweep(F, nLb);
-  acc_rz = fwd_sweep(F, nLf);
-  rz = wsum(acc_rz);
+  rz = wsum(fwd_sweep(F, nLf));
 }
 
 struct PcgResult {
   int iters, status;
-  double relres;
+  double relres;       // TRUE ||w - Q dy|| / ||w|| at exit
+  double rec_relres;   // recursive ||r|| / ||w|| at exit of the last recursion
 };
 
 // l = Q h = A (D^2 (A^T h)) matrix-free over the edges (eq.`Delta y` LHS), h in
@@ -1010,57 +1012,68 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
   return ABS ? 0.0 : wsum(hl);
 }
 
-// One PCG run (Alg. 4) in preconditioner mode `mode`, from dy = 0, r = w.
-// The recursion stops after line 9 once ||r||_2 <= tol (G15); the TRUE residual w - Q dy is
-// then evaluated and must pass the same test.  Outcomes: 0 converged, ST_PCG_FLOOR (true
-// residual at the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||), ST_PCG_MAXITER,
-// ST_PCG_BREAKDOWN (h^T Q h or z^T r not > 0 / non-finite, the recursive residual
-// diverging 1e8-fold, or — MTS mode — no new minimum in 200 iterations).  ST_PCG_FLOOR also
-// ends a refinement restart that no longer halves the true residual within 1e3x of the floor.  When the
-// recursion converges but the true residual fails the test, the run restarts from the
-// true residual (iterative refinement with the same preconditioner), at most 4 times.
-// `it` accumulates iterations across runs.
-__device__ ALP_HEAVY int pcg_run(const Frame& F, const Params& P, int mode, int nLb, int nLf, double wn,
-                       int& it, int cap, double& relres, double rel_tol, double inner_tol) {
+// PCG (Alg. 4) from dy = 0, r = w, in preconditioner mode `mode`.  The recursion
+// stops after line 9 once ||r||_2 <= itol ||w||_2 (G15, C-9; itol <= pcg_rel_tol is the
+// inexact-Newton target of the caller); once ||r|| <= pcg_rel_tol ||w|| (the acceptance test of
+// C-9) the recursion gets at most 50 more iterations towards itol.  It also ends at the cap, on a
+// breakdown (h^T Q h or z^T r not > 0 / non-finite; both are sums of squares, so only 0 / inf /
+// nan), or on a stall (no new minimum of ||r|| in 200 iterations for MTS, 1000 for CG, or
+// 1e8-fold growth; R-1).  The TRUE residual w - Q dy is then evaluated once.
+// `refine` (ipm_step_pcg only): while the true residual fails pcg_rel_tol, restart from it
+// (iterative refinement with the same preconditioner, at most 4 restarts); a restart that no
+// longer halves it within 1e3x of the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||
+// stops with ST_PCG_FLOOR (attainable accuracy, informational).
+// Status: 0 = the last recursion met pcg_rel_tol (P4), ST_PCG_MAXITER (cap or stall),
+// ST_PCG_BREAKDOWN, ST_PCG_FLOOR (refine mode).  w is read from F.w; dy accumulates in F.dy.
+__device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mode, int nLb, int nLf,
+                                         double itol_rel, bool refine) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
   double* hS = F.S<double>(L.s_h);
   double* rS = F.S<double>(L.s_r);
-  const double tol = rel_tol * wn;            // acceptance on the true residual
-  const double itol = fmin(inner_tol, rel_tol) * wn;   // recursion target
   double* zS = F.S<double>(L.s_z);
   double* fS = F.S<double>(L.s_f);
+  double ww = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
-    bool pr = (F.sgnC[j] & PRESENT) != 0;
-    rS[j] = pr ? F.w[j] : 0.0;   // lines 1-2: x^0 = 0, r^0 = w
+    const bool pr = (F.sgnC[j] & PRESENT) != 0;
+    const double wj = pr ? F.w[j] : 0.0;
+    ww += wj * wj;
+    rS[j] = wj;        // lines 1-2: x^0 = 0, r^0 = w
     F.dy[j] = 0.0;
-    zS[j] = 0.0;                 // absent rows stay exactly 0 in z, f and h (C-19)
+    zS[j] = 0.0;       // absent rows stay exactly 0 in z, f and h (C-19)
     fS[j] = 0.0;
   }
   __syncwarp();
-  relres = 1.0;
+  const double wn = sqrt(wsum(ww));
+  PcgResult res{0, 0, 0.0, 0.0};
+  if (wn == 0.0) return res;
+  const double tol = P.pcg_rel_tol * wn;                       // acceptance (C-9)
+  const double itol = fmin(itol_rel, P.pcg_rel_tol) * wn;      // recursion target
+  const int cap = P.pcg_max_iter;
+  int it = 0;
   double prev_trn = 1e308;
-  for (int restart = 0; restart <= 4; ++restart) {
+  for (int restart = 0; restart <= (refine ? 4 : 0); ++restart) {
     double rz;
     precond_apply(F, mode, nLb, nLf, rz);   // line 3
-    if (!(rz > 0.0) || !isfinite(rz)) return ST_PCG_BREAKDOWN;
+    if (!(rz > 0.0) || !isfinite(rz)) {
+      res.status = ST_PCG_BREAKDOWN;
+      break;
+    }
     for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? zS[j] : 0.0;   // line 4
     __syncwarp();
-    bool conv = false, bad = false;
-    int past = -1;
-    double rrmin = 1e308;
-    int since_min = 0;
+    int st = ST_PCG_MAXITER, past = -1, since_min = 0;
+    double rrmin = 1e308, rr = 0.0;
     long long tk = clock64();
     while (it < cap) {
       ALP_TICK(F, CY_PCG, tk);
-      double hl = spmv<false>(F);   // line 6: l = Q h
+      const double hl = spmv<false>(F);   // line 6: l = Q h
       ALP_TICK(F, CY_SPMV, tk);
       if (!(hl > 0.0) || !isfinite(hl)) {
-        bad = true;
+        st = ST_PCG_BREAKDOWN;
         break;
       }
       const double alpha = rz / hl;   // line 7
-      double rr = 0.0;
+      double acc = 0.0;
       {
         double* __restrict__ dyp = F.dy;
         const double* __restrict__ lp = F.l;
@@ -1068,25 +1081,24 @@ __device__ ALP_HEAVY int pcg_run(const Frame& F, const Params& P, int mode, int 
 #pragma unroll 4
         for (int j = F.lane; j < C.m; j += 32) {
           if (!(sc[j] & PRESENT)) continue;
-          dyp[j] += alpha * hS[j];   // line 8
-          double r = rS[j] - alpha * lp[j];   // line 9
+          dyp[j] += alpha * hS[j];             // line 8
+          const double r = rS[j] - alpha * lp[j];   // line 9
           rS[j] = r;
-          rr += r * r;
+          acc += r * r;
         }
       }
       __syncwarp();
-      rr = wsum(rr);
+      rr = wsum(acc);
       ++it;
-      if (sqrt(rr) <= itol) {
-        conv = true;
+      const double rn = sqrt(rr);
+      if (rn <= itol) {
+        st = 0;
         break;
       }
-      // past the acceptance tolerance, the forcing-term target gets at most 50 more iterations
-      // (an unreachable target would otherwise let the recursion drift, R-1)
-      if (sqrt(rr) <= tol) {
+      if (rn <= tol) {   // accepted; at most 50 more iterations towards the forcing target
         if (past < 0) past = it;
         else if (it - past >= 50) {
-          conv = true;
+          st = 0;
           break;
         }
       }
@@ -1094,21 +1106,15 @@ __device__ ALP_HEAVY int pcg_run(const Frame& F, const Params& P, int mode, int 
         rrmin = rr;
         since_min = 0;
       } else if (rr > 1e16 * rrmin || ++since_min > (mode == PC_MTS ? 200 : 1000)) {
-        if (rrmin <= tol * tol) {   // stalled below the acceptance tolerance: good enough
-          conv = true;
-          break;
-        }
-        if (mode == PC_MTS) {
-          bad = true;
-          break;
-        }
+        st = (rrmin <= tol * tol) ? 0 : ST_PCG_MAXITER;   // stall
+        break;
       }
       double rz_new;
       ALP_TICK(F, CY_PCG, tk);
       precond_apply(F, mode, nLb, nLf, rz_new);   // line 10
       ALP_TICK(F, CY_SWEEP, tk);
       if (!(rz_new > 0.0) || !isfinite(rz_new)) {
-        bad = true;
+        st = ST_PCG_BREAKDOWN;
         break;
       }
       const double nu = rz_new / rz;   // line 11
@@ -1121,115 +1127,39 @@ __device__ ALP_HEAVY int pcg_run(const Frame& F, const Params& P, int mode, int 
       __syncwarp();
     }
     ALP_TICK(F, CY_PCG, tk);
-    if (bad) return ST_PCG_BREAKDOWN;
-    // true residual r = w - Q dy (h <- dy; h is rebuilt on restart)
+    res.rec_relres = sqrt(rr) / wn;
+    if (st == 0 && !(res.rec_relres <= P.pcg_rel_tol)) st = ST_PCG_MAXITER;
+    // TRUE residual r = w - Q dy (h <- dy; h is rebuilt on a restart)
     for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
     __syncwarp();
     spmv<false>(F);
-    double rr = 0.0;
+    double tr = 0.0;
     for (int j = F.lane; j < C.m; j += 32) {
       double r = 0.0;
       if (F.sgnC[j] & PRESENT) r = F.w[j] - F.l[j];
       rS[j] = r;
-      rr += r * r;
+      tr += r * r;
     }
     __syncwarp();
-    const double trn = sqrt(wsum(rr));
-    relres = trn / wn;
-    if (!isfinite(trn)) return ST_PCG_BREAKDOWN;
-    if (trn <= tol) return 0;
-    // attainable-accuracy floor of the residual evaluation itself
-    spmv<true>(F);
+    const double trn = sqrt(wsum(tr));
+    res.relres = trn / wn;
+    res.status = st;
+    ALP_TICK(F, CY_PCG, tk);
+    if (!refine || st == ST_PCG_BREAKDOWN || !isfinite(trn)) break;
+    if (trn <= tol) break;   // the true residual meets C-9
+    spmv<true>(F);           // attainable-accuracy floor of the residual evaluation itself
     double aa = 0.0;
     for (int j = F.lane; j < C.m; j += 32)
       if (F.sgnC[j] & PRESENT) aa += F.l[j] * F.l[j];
-    aa = sqrt(wsum(aa));
-    const double floor_est = 16.0 * 2.220446049250313e-16 * aa;
-    if (trn <= floor_est) return ST_PCG_FLOOR;
-    if (!conv) return ST_PCG_MAXITER;
-    // The recursion converged but the true residual did not: restart from it (iterative
-    // refinement with the same preconditioner).  A restart that does not halve the true
-    // residual while it is within 1e3x of the evaluation-floor estimate has reached the
-    // attainable fp64 accuracy: stop there (ST_PCG_FLOOR).
-    if (trn > 0.5 * prev_trn && trn <= 1e3 * floor_est) return ST_PCG_FLOOR;
+    const double floor_est = 16.0 * 2.220446049250313e-16 * sqrt(wsum(aa));
+    if (trn <= floor_est || (trn > 0.5 * prev_trn && trn <= 1e3 * floor_est)) {
+      res.status = (st == 0) ? ST_PCG_FLOOR : st;
+      break;
+    }
+    if (st != 0) break;     // the recursion itself failed: no refinement
     prev_trn = trn;
   }
-  return ST_PCG_MAXITER;
-}
-
-// 1/diag(Q), diag(Q)_j = sum_{i in N(j)} d2_i + d2_{n+j} (A entries are +-1), into dinvF
-// (the MTS sweep program's scale factors are dead once a solve falls back).
-__device__ void jacobi_setup(const Frame& F) {
-  const DCode& C = *F.C;
-  for (int j = F.lane; j < C.m; j += 32) {
-    double dq = 0.0;
-    if (F.sgnC[j] & PRESENT) {
-      dq = F.d2[C.n + j];
-      int deg = C.chk_deg[j];
-      for (int t = 0; t < deg; ++t) dq += F.d2[chk_nb(C, j, t)];
-    }
-    F.dinvF[j] = (dq > 0.0) ? 1.0 / dq : 0.0;
-  }
-  __syncwarp();
-}
-
-// Step solve of eq.`Delta y` by PCG.  precond = 0: the paper's column-wise MTS
-// preconditioner (Alg. 7).  Late in the IPM the column-wise set need not contain the
-// basic columns (Remark P:807-810); kappa(M^-1 Q) then explodes and the fp64 recursion
-// decouples from the true residual.  So (R-2): an MTS run that breaks down,
-// stalls or hits the cap — or, inside the IPM (floor_accept = 1e-6), ends at a floor above
-// 1e-6 ||w|| — is followed by a Jacobi-preconditioned CG run from dy = 0 to
-// pcg_fallback_tol (ST_PCG_FALLBACK, informational) within the iteration cap, and the
-// better of the two results is kept.  precond = 1: plain CG only.
-// w is read from F.w; the solution is left in F.dy.
-__device__ PcgResult pcg_solve(const Frame& F, const Params& P, bool use_mtm, int nLb, int nLf,
-                               double inner_tol, double floor_accept) {
-  const DCode& C = *F.C;
-  double ww = 0.0;
-  for (int j = F.lane; j < C.m; j += 32) {
-    double wj = (F.sgnC[j] & PRESENT) ? F.w[j] : 0.0;
-    ww += wj * wj;
-    F.dy[j] = 0.0;
-  }
-  __syncwarp();
-  const double wn = sqrt(wsum(ww));
-  PcgResult res{0, 0, 0.0};
-  if (wn == 0.0) return res;
-  int it = 0;
-  if (!use_mtm) {
-    res.status = pcg_run(F, P, PC_NONE, 0, 0, wn, it, P.pcg_max_iter, res.relres, P.pcg_rel_tol,
-                         inner_tol);
-    res.iters = it;
-    return res;
-  }
-  double rel1 = 1.0;
-  int st1 = pcg_run(F, P, PC_MTS, nLb, nLf, wn, it, P.pcg_max_iter, rel1, P.pcg_rel_tol, inner_tol);
-  if (st1 == 0 || (st1 == ST_PCG_FLOOR && rel1 <= floor_accept) || !P.pcg_fallback) {
-    res.status = st1;
-    res.relres = rel1;
-    res.iters = it;
-    return res;
-  }
-  const bool keep1 = (st1 == ST_PCG_FLOOR);   // a usable floor-limited MTS result
-  if (keep1)
-    for (int j = F.lane; j < C.m; j += 32) F.dyb[j] = F.dy[j];
-  __syncwarp();
-  jacobi_setup(F);
-  int it2 = 0;
-  double rel2 = 1.0;
-  int st2 = pcg_run(F, P, PC_JACOBI, 0, 0, wn, it2, P.pcg_max_iter, rel2, P.pcg_fallback_tol,
-                    inner_tol);
-  res.iters = it + it2;
-  if (st2 != 0 && st2 != ST_PCG_BREAKDOWN && rel2 <= P.pcg_rel_tol) st2 = 0;   // met the C-9 test
-  if (keep1 && (st2 != 0) && !(st2 == ST_PCG_FLOOR && rel2 <= rel1)) {
-    for (int j = F.lane; j < C.m; j += 32) F.dy[j] = F.dyb[j];
-    __syncwarp();
-    res.status = st1 | ST_PCG_FALLBACK;
-    res.relres = rel1;
-  } else {
-    res.status = st2 | ST_PCG_FALLBACK;
-    res.relres = rel2;
-  }
+  res.iters = it;
   return res;
 }
 

@@ -14,8 +14,11 @@ import torch
 import torch.distributed as dist
 
 # order of the counter vector reduced at the end of a run
+STATUS_BITS = {"alp_maxiter": 1, "ipm_maxiter": 2, "pcg_maxiter": 4, "pcg_breakdown": 8, "numeric": 16}
 COUNTERS = ("frames", "frame_errors", "not_certified", "lp_solves", "ipm_iters", "pcg_iters",
-            "status_nonzero", "pcg_bytes")
+            "frames_capped", "pcg_bytes", "pcg_solves", "pcg_p4_failed_solves",
+            "pcg_true_failed_solves") + tuple("frames_" + k for k in STATUS_BITS)
+CAP_BITS = 1 | 2 | 16
 
 
 def shard_frame_ids(frames_per_rank: int, rank: int, world_size: int) -> np.ndarray:
@@ -26,13 +29,23 @@ def shard_frame_ids(frames_per_rank: int, rank: int, world_size: int) -> np.ndar
 
 
 def frame_counters(hard, codewords, certificate, status, stats) -> np.ndarray:
-    """Per-rank counter vector (COUNTERS order) from one decode's host-side outputs."""
+    """Per-rank counter vector (COUNTERS order) from one decode's host-side outputs.
+    frames_capped = frames whose decode ended on a cap / cycle / non-finite status; the
+    frames_<bit> entries count the frames carrying each alp_frame_status bit."""
     hard = np.asarray(hard)
+    status = np.asarray(status)
     errs = int(np.any(hard != np.asarray(codewords), axis=1).sum())
+    bits = [int(((status & b) != 0).sum()) for b in STATUS_BITS.values()]
     return np.array([hard.shape[0], errs, int((np.asarray(certificate) == 0).sum()),
                      int(stats["lp_solves"].sum()), int(stats["ipm_iters"].sum()),
-                     int(stats["pcg_iters"].sum()), int((np.asarray(status) != 0).sum()),
-                     float(stats["pcg_bytes"].sum())], dtype=np.float64)
+                     int(stats["pcg_iters"].sum()), int(((status & CAP_BITS) != 0).sum()),
+                     float(stats["pcg_bytes"].sum()), int(stats["pcg_solves"].sum()),
+                     int(stats["pcg_p4_fail"].sum()), int(stats["pcg_true_fail"].sum())] + bits,
+                    dtype=np.float64)
+
+
+def counters_dict(c) -> dict:
+    return {k: (float(v) if k == "pcg_bytes" else int(v)) for k, v in zip(COUNTERS, c)}
 
 
 def reduce_run(counters: np.ndarray, seconds: float, device=None) -> tuple[np.ndarray, float]:

@@ -64,7 +64,7 @@ int main(void) {
         vals = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
     assert vals == [C.sizeof(AlpParams), AlpParams.sigma.offset, AlpParams.alp_max_iter.offset,
                     AlpParams.warps_per_block.offset, C.sizeof(FrameStats)]
-    assert C.sizeof(FrameStats) == 96
+    assert C.sizeof(FrameStats) == 128
 
 
 def test_default_params_equal_oracle_constants(lib):

@@ -24,16 +24,22 @@ def test_shards_partition_the_frames():
 
 
 def test_frame_counters():
-    st = np.zeros(3, dtype=[("lp_solves", "<i4"), ("ipm_iters", "<i4"), ("pcg_iters", "<i4"),
-                            ("pcg_bytes", "<f8")])
+    from paper_0902_0657_b200._ffi import STATS_FIELDS
+    st = np.zeros(3, dtype=STATS_FIELDS)
     st["lp_solves"] = [1, 2, 3]
     st["pcg_iters"] = [10, 0, 5]
     st["pcg_bytes"] = [1.5, 0, 2.5]
+    st["pcg_solves"] = [4, 0, 2]
+    st["pcg_p4_fail"] = [1, 0, 0]
     hard = np.array([[0, 1], [1, 1], [0, 0]])
     cw = np.array([[0, 1], [0, 1], [0, 0]])
-    c = frame_counters(hard, cw, [1, 0, 1], [0, 0, 4], st)
-    assert dict(zip(COUNTERS, c)) == dict(frames=3, frame_errors=1, not_certified=1, lp_solves=6,
-                                          ipm_iters=0, pcg_iters=15, status_nonzero=1, pcg_bytes=4.0)
+    c = frame_counters(hard, cw, [1, 0, 1], [0, 2 | 4, 4], st)
+    d = dict(zip(COUNTERS, c))
+    assert d == dict(frames=3, frame_errors=1, not_certified=1, lp_solves=6, ipm_iters=0,
+                     pcg_iters=15, frames_capped=1, pcg_bytes=4.0, pcg_solves=6,
+                     pcg_p4_failed_solves=1, pcg_true_failed_solves=0, frames_alp_maxiter=0,
+                     frames_ipm_maxiter=1, frames_pcg_maxiter=2, frames_pcg_breakdown=0,
+                     frames_numeric=0)
 
 
 def _worker(rank, ws, port, q):

@@ -74,7 +74,7 @@ for label, snr in (("integral_1.5dB", 1.5), ("fractional_1.0dB", 1.0)):
         for name, pc in (("column-wise MTS", 0), ("CG", 1)):
             res = []
             for k in range(1, K + 1):
-                prm = alp.default_params(precond=pc, pcg_max_iter=k, pcg_rel_tol=1e-14, pcg_fallback=0)
+                prm = alp.default_params(precond=pc, pcg_max_iter=k, pcg_rel_tol=1e-14)
                 sol = alp.ipm_step_pcg(c, tm, td, tr, params=prm)
                 torch.cuda.synchronize()
                 y = sol.dy.cpu().numpy()[0][rows]
