@@ -131,12 +131,15 @@ typedef struct {
   int32_t warps_per_block;/* tuning: frames (one warp each) per CTA; 0 = automatic             */
   int32_t smem_frames_per_sm; /* tuning: resident frames per SM the shared-memory budget is split
                              over; hot PCG arrays move into shared memory while they fit;
-                             0 = automatic (11: measured best; a small window keeps L1 large) */
+                             0 = automatic (8: measured best, tools/tune_smem.py)          */
   int32_t stop_on_lp_failure; /* 1: a frame stops decoding after an LP whose IPM hit
                              ipm_max_iter (reading C-30; status bit set, last u output)  1      */
   int32_t basis_correction; /* 1: after each Newton step the primal residual rho = r_b - A dx
                              left by an inexact PCG dy is removed on the preconditioner's
                              basis columns (A_M f = rho, dx_M += f; reading C-32)        1      */
+  double pcg_forcing;     /* inexact-Newton forcing factor: inside the IPM the PCG recursion
+                             aims at min(pcg_rel_tol, pcg_forcing * mu) (R-1); 0 =
+                             plain pcg_rel_tol                                         1e-2   */
 } alp_params;
 
 /* Fills the defaults listed above (identical to the oracle's constants). */
@@ -206,8 +209,9 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
                         int32_t* pivot_rows, int32_t* pivot_cols, void* workspace,
                         size_t workspace_bytes, const alp_params* params, void* stream);
 
-/* Diagnostics: when `records` (DEVICE, capacity x 80-byte records {int32 frame, lp, ipm_it,
- * p, status, pcg_iters; fp64 relres, d2_min, d2_max, mu, ||r_b||inf, ||r_c||inf, gap}) is non-NULL, every subsequent
+/* Diagnostics: when `records` (DEVICE, capacity x 104-byte records {int32 frame, lp, ipm_it,
+ * p, status, pcg_iters; fp64 true relres, recursive relres, d2_min, d2_max, mu, ||r_b||inf,
+ * ||r_c||inf, gap, beta_P, beta_D}) is non-NULL, every subsequent
  * alp_decode appends one record per Newton-step solve (order unspecified, records beyond
  * capacity dropped).  NULL disables.  Process-wide; not thread safe; not for production. */
 alp_status alp_debug_trace(void* records, int32_t capacity);

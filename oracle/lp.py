@@ -27,6 +27,7 @@ import scipy.linalg as sla
 import scipy.sparse as sp
 
 PRESENT = 1 << 15
+SPARSE_Q = 8192     # LPs with more columns keep A in sparse storage (config 4; same products)
 
 # DESIGN.md §3 / SURVEY.md §8(c) c.3 constants (C-3, C-4, C-5, C-6, C-8, C-9, C-11, C-12)
 DEFAULT_PARAMS = dict(
@@ -101,7 +102,8 @@ def augmented_lp(code, pool: dict, gamma: np.ndarray):
     (eq.`constraints`, P:107-110) with u_i = x_i (gamma_i >= 0) or u_i = 1 - x_i
     (gamma_i < 0) becomes sum_i a_ji s_i x_i + x_{n+r} = |V| - 1 - sum_{i flipped} a_ji,
     a_ji = +1 on V, -1 off V, s_i = -1 if flipped.  Cost c_i = |gamma_i|, slack cost 0.
-    Returns dict with dense A (p x q), b (p), c (q), rows (check ids), flip, const
+    Returns dict with A (p x q; dense, or scipy.sparse CSR when q > SPARSE_Q — storage only,
+    for config 4), b (p), c (q), rows (check ids), flip, const
     (= sum_{gamma_i<0} gamma_i so that gamma^T u = c^T x + const).
     """
     gamma = np.asarray(gamma, dtype=np.float64)
@@ -110,16 +112,20 @@ def augmented_lp(code, pool: dict, gamma: np.ndarray):
     rows = sorted(pool.keys())
     p = len(rows)
     q = n + p
-    A = np.zeros((p, q))
+    ri, ci, vals = [], [], []
     b = np.zeros(p)
     for r, j in enumerate(rows):
         Nj = code.N(j)
         inV = np.asarray(pool[j], dtype=bool)
         a = np.where(inV, 1.0, -1.0)
         s = np.where(flip[Nj], -1.0, 1.0)
-        A[r, Nj] = a * s
-        A[r, n + r] = 1.0
+        ri += [r] * (len(Nj) + 1)
+        ci += list(Nj) + [n + r]
+        vals += list(a * s) + [1.0]
         b[r] = inV.sum() - 1.0 - np.sum(a[flip[Nj]])
+    A = sp.csr_matrix((vals, (ri, ci)), shape=(p, q))
+    if q <= SPARSE_Q:
+        A = A.toarray()
     c = np.concatenate([np.abs(gamma), np.zeros(p)])
     const = float(np.sum(gamma[flip]))
     return dict(A=A, b=b, c=c, rows=rows, flip=flip, n=n, p=p, q=q, const=const)
@@ -263,9 +269,9 @@ def ipm_solve(A, b, c, params=None, step_solver=None, record=False):
     At most ipm_max_iter Newton steps.
     """
     P = dict(DEFAULT_PARAMS) if params is None else params
-    A = np.asarray(A, dtype=np.float64)
+    A = sp.csr_matrix(A, dtype=np.float64) if sp.issparse(A) else np.asarray(A, dtype=np.float64)
     p, q = A.shape
-    if q > 256:
+    if q > 256 and not sp.issparse(A):
         A = sp.csr_matrix(A)   # storage only; every product below is unchanged
     b = np.asarray(b, dtype=np.float64)
     c = np.asarray(c, dtype=np.float64)

@@ -17,7 +17,7 @@ class AlpParams(C.Structure):
         ("alp_max_iter", C.c_int32), ("ipm_max_iter", C.c_int32), ("pcg_max_iter", C.c_int32),
         ("warps_per_block", C.c_int32), ("smem_frames_per_sm", C.c_int32),
         ("stop_on_lp_failure", C.c_int32),
-        ("basis_correction", C.c_int32),
+        ("basis_correction", C.c_int32), ("pcg_forcing", C.c_double),
     ]
 
 
@@ -70,11 +70,13 @@ SIGNATURES = {
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Loads libalp.so; raises (never falls back) when it is missing."""
+def load(path: str | None = None):
+    """Loads libalp.so; raises (never falls back) when it is missing.  ALP_LIB (diagnostics
+    only) points at another build of the same library, e.g. a tuning variant."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("ALP_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"libalp.so not built at {path}: run `python -m paper_0902_0657_b200.build` "
                           "(or __graft_entry__.build()); there is no CPU fallback")

@@ -34,20 +34,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compiles libalp.so (or, for tuning experiments, a variant `out` with extra -D defines)."""
+    target = out or OUT
+    if not force and out is None and not needs_build():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *SRC]
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-o", target + ".tmp", *SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libalp.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(res.stderr)
-    return OUT
+    os.replace(target + ".tmp", target)
+    if out is None:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+            fh.write(res.stderr)
+    return target
 
 
 if __name__ == "__main__":

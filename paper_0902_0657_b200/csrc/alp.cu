@@ -19,7 +19,7 @@ namespace alp {
 // Optional per-Newton-step trace (alp_debug_trace): one record per step solve.
 struct TraceRec {
   int frame, lp, ipm_it, p, status, iters;
-  double relres, d2min, d2max, mu, rb, rc, gap;
+  double relres, rec_relres, d2min, d2max, mu, rb, rc, gap, beta_p, beta_d;
 };
 __device__ TraceRec* g_trace = nullptr;
 __device__ int g_trace_cap = 0;
@@ -162,7 +162,7 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); P4 acceptance is pcg_rel_tol.  An inexact
     // dy is admissible because the recovery below keeps every KKT row but the complementarity
     // of the basis columns exact (C-32).
-    const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, 1e-2 * mu));
+    const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, P.pcg_forcing * mu));
     PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, inner, false);
     tk = clock64();
     out.status |= pr.status;
@@ -171,8 +171,8 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     out.true_fail += (pr.relres > P.pcg_rel_tol) ? 1 : 0;
     out.max_rec = fmax(out.max_rec, pr.rec_relres);
     out.max_true = fmax(out.max_true, pr.relres);
+    double dmn = 1e308, dmx = 0.0;
     if (g_trace) {
-      double dmn = 1e308, dmx = 0.0;
       for (int c = lane; c < Q; c += 32) {
         if (c >= n && !(SC[c - n] & PRESENT)) continue;
         dmn = fmin(dmn, D2[c]);
@@ -180,11 +180,6 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
       }
       dmn = wmin(dmn);
       dmx = wmax(dmx);
-      if (lane == 0) {
-        int slot = atomicAdd(&g_trace_n, 1);
-        if (slot < g_trace_cap)
-          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, pr.relres, dmn, dmx, mu, rbn, rcn, gap};
-      }
     }
     out.pcg_iters += pr.iters;
     out.pcg_bytes += (double)pr.iters * Bmin;
@@ -256,6 +251,13 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     az = wmin(az);
     const double bP = fmin(1.0, P.eta * ax);
     const double bD = fmin(1.0, P.eta * az);
+    if (g_trace) {
+      if (lane == 0) {
+        int slot = atomicAdd(&g_trace_n, 1);
+        if (slot < g_trace_cap)
+          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, pr.relres, pr.rec_relres, dmn, dmx, mu, rbn, rcn, gap, bP, bD};
+      }
+    }
     bool bad = false;
 #pragma unroll 4
     for (int c = lane; c < Q; c += 32) {
@@ -438,7 +440,10 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
+#ifndef ALP_MINB
+#define ALP_MINB 1
+#endif
+__global__ void __launch_bounds__(128, ALP_MINB) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
                                                         char* slots,
                                                         const double* __restrict__ llr,
                                                         long long n_frames, DecodeOut O,
@@ -454,7 +459,8 @@ __global__ void __launch_bounds__(128) alp_decode_kernel(DCode C, Params P, Layo
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   Frame F;
-  frame_bind(F, &sC, &sL, slots + gw * L.slot_bytes, smem + G.bytes + warp * L.smem_bytes, lane);
+  char* slot = slots + gw * L.slot_bytes;
+  frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
   __shared__ long long s_cyc[4][8];   // phase clocks in shared memory (a global RMW per tick
   F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
   while (true) {
@@ -494,7 +500,8 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   Frame F;
-  frame_bind(F, &sC, &sL, slots + gw * L.slot_bytes, smem + G.bytes + warp * L.smem_bytes, lane);
+  char* slot = slots + gw * L.slot_bytes;
+  frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
   const int n = C.n, m = C.m, Q = C.Q;
   while (true) {
     long long s = 0;
@@ -565,11 +572,6 @@ alp_status cuda_fail(cudaError_t e, const char* what) {
   return fail(ALP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 size_t al(size_t x, size_t a = 16) { return (x + a - 1) / a * a; }
-int pow2ceil(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
 
 DCode make_dcode(const alp_code* c) {
   DCode C;
@@ -578,7 +580,6 @@ DCode make_dcode(const alp_code* c) {
   C.dc = c->dc;
   C.dv = c->dv;
   C.Q = c->n + c->m;
-  C.QP2 = pow2ceil(C.Q);
   C.W = (C.Q + 63) / 64;
   C.RB = (int)al(1 + c->dc, 4);
   C.chk_var = c->d_chk_var;
@@ -624,8 +625,6 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.g_pcol = g(2 * m);
   L.slot_bytes = (long long)al(o, 256);
   // shared window
-  size_t s_sort = 8 * (size_t)C.QP2;
-  L.s_keys = 0;
   size_t a = 0;
   auto s = [&](size_t bytes) {
     size_t r = a;
@@ -633,6 +632,12 @@ Layout make_layout(const DCode& C, int smem_budget) {
     return (int)r;
   };
   L.s_order = s(2 * Q);
+  // sort phase (radix buffers kA/kB u32[Q], cA/cB u16[Q], 256-bin histogram) after `order`
+  const size_t sort_base = a;
+  L.s_sortk = (int)sort_base;
+  L.s_sorth = (int)(sort_base + al(12 * Q, 16));
+  const size_t s_sort = sort_base + al(12 * Q, 16) + 1024;
+  a = sort_base;
   L.s_rank = s(2 * Q);
   L.s_cnt = s(Q);
   L.s_xr = s(2 * Q);
@@ -668,6 +673,18 @@ Layout make_layout(const DCode& C, int smem_budget) {
     end_pcg = a;
   }
   size_t tot = al(std::max(s_sort, std::max(end_peel, end_pcg)), 16);
+  L.win_global = 0;
+  L.g_win = 0;
+  if ((long long)tot > (long long)smem_budget) {
+    // large code: the whole phase window goes to the slot (global memory, L2-cached), nothing
+    // is relocated, and the kernel needs no per-frame shared memory
+    L.win_global = 1;
+    L.g_win = (long long)al(o, 256);
+    L.slot_bytes = (long long)al(L.g_win + tot, 256);
+    L.smask = 0;
+    L.smem_bytes = 0;
+    return L;
+  }
   // Relocate the arrays the PCG loop touches every iteration into the shared window, by
   // priority (sign tables, l, dy, sweep program, D^2, w), while the window fits the budget.
   L.smask = 0;
@@ -719,7 +736,9 @@ int smem_budget_for(const alp_params* p) {
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
     optin = 227 * 1024;
-  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 11;
+  // measured (tools/tune_smem.py, C2 3.0 dB, round 2): 8 beats 11 by ~25 % — the PCG vectors
+  // and sweep programs then live in shared memory, worth more than the L1 the window takes
+  int fps = (p && p->smem_frames_per_sm > 0) ? p->smem_frames_per_sm : 8;
   return (optin / fps) & ~127;
 }
 
@@ -737,6 +756,7 @@ Params make_params(const alp_params* p) {
   P.pcg_rel_tol = p->pcg_rel_tol;
   P.stop_on_lp_failure = p->stop_on_lp_failure;
   P.basis_correction = p->basis_correction;
+  P.pcg_forcing = p->pcg_forcing;
   P.tau_viol = p->tau_viol;
   P.tau_act = p->tau_act;
   P.tau_cert = p->tau_cert;
@@ -838,6 +858,7 @@ void alp_default_params(alp_params* p) {
   p->smem_frames_per_sm = 0;
   p->stop_on_lp_failure = 1;
   p->basis_correction = 1;
+  p->pcg_forcing = 1e-2;
 }
 
 const char* alp_status_string(alp_status s) {

@@ -35,14 +35,14 @@ constexpr int ST_ALP_MAXITER = 1, ST_IPM_MAXITER = 2, ST_PCG_MAXITER = 4, ST_PCG
 
 struct Params {
   int variant, precond;
-  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, tau_viol, tau_act, tau_cert;
+  double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, pcg_forcing, tau_viol, tau_act, tau_cert;
   int alp_max_iter, ipm_max_iter, pcg_max_iter;
   int stop_on_lp_failure, basis_correction;
 };
 
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
 struct DCode {
-  int n, m, dc, dv, Q, QP2, W, RB;        // Q = n + m columns, QP2 = pow2 >= Q, W = bitmap words
+  int n, m, dc, dv, Q, W, RB;             // Q = n + m columns, W = bitmap words
   const uint16_t* __restrict__ chk_var;   // [m][dc] sorted variables of each check, 0xffff padded
   const uint8_t* __restrict__ chk_deg;    // [m]
   const uint16_t* __restrict__ var_chk;   // [n][dv] checks of each variable, 0xffff padded
@@ -83,11 +83,15 @@ struct Layout {
   long long g_cyc, g_x, g_z, g_d2, g_v, g_y, g_dy, g_l, g_w, g_u, g_b, g_dinvF, g_recB, g_recF, g_offB,
       g_offF, g_sgnC, g_mask, g_hist, g_sgnV, g_flip, g_rb, g_rc, g_pcol;
   int smem_bytes;
+  // win_global: the phase window does not fit the shared-memory budget (large codes, e.g.
+  // config 4): it lives in the slot at g_win and is addressed through the same generic pointers
+  int win_global;
+  long long g_win;
   // Hot per-frame arrays that live in the warp's shared window instead of the slot
   // (bit k of smask set <=> array k at shared offset soff[k]); order = placement priority.
   unsigned smask;
   int soff[12];
-  int s_keys;                                                                  // sort phase
+  int s_sortk, s_sorth;                                                        // sort phase
   int s_order, s_rank, s_cnt, s_xr, s_bm, s_pos, s_pcol, s_prow, s_lvB, s_lvF;  // peel phase
   int s_poc, s_hist, s_cur;                                                    // post-peel
   int s_h, s_r, s_f, s_z, s_t;                                                 // PCG phase
@@ -326,165 +330,208 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
 // =====================================================================================
 // Preconditioner build, part 1: rank the columns by weight (Alg. 7 needs "the maximum
 // weight d_i" among DEG1; weight d^2 = x/z gives the same order, C-10).
-// Packed 64-bit keys (~float(d^2) bits << 32 | column) sorted ascending by a warp bitonic
-// sort in shared memory = descending float weight, ascending column; runs of equal float
-// keys are then re-ordered by the exact fp64 weight (ties -> lower column).  Columns
-// without a present row (degree 0 in the extended Tanner graph) sort last.
+// Valid columns (>= 1 present row; degree 0 in the extended Tanner graph otherwise) are
+// compacted in ascending column order with the 32-bit key ~bits(float(d^2)) (ascending key =
+// descending weight), then a stable LSD radix sort (4 passes of 8 bits, passes whose digit is
+// the same for every key skipped) orders them: descending float weight, ascending column on
+// equal floats.  Runs of equal float keys are then re-ordered by the exact fp64 weight (ties
+// -> lower column).  Result: order[r] = column of rank r (r < nv), returns nv.
+// Buffers (shared window, sort phase): kA/kB u32[Q], cA/cB u16[Q], hist u32[256]; order
+// u16[Q] must not overlap them (layout: s_order, then s_sortk).
 // =====================================================================================
-__device__ ALP_HEAVY void sort_columns(const Frame& F) {
+__device__ ALP_HEAVY int sort_columns(const Frame& F) {
   const DCode& C = *F.C;
-  uint64_t* keys = F.S<uint64_t>(F.L->s_keys);
-  // valid columns (>= 1 present row) are compacted to the front (warp ballot prefix), the rest
-  // of the key array is padding (~0); only the next power of two >= #valid is sorted
-  int nv = 0;
+  const Layout& L = *F.L;
+  uint32_t* kA = F.S<uint32_t>(L.s_sortk);
+  uint32_t* kB = kA + C.Q;
+  uint16_t* cA = reinterpret_cast<uint16_t*>(kB + C.Q);
+  uint16_t* cB = cA + C.Q;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(F.sm + L.s_sorth);
+  uint16_t* order = F.S<uint16_t>(L.s_order);
   const unsigned lt = (1u << F.lane) - 1u;
+  int nv = 0;
   for (int c0 = 0; c0 < C.Q; c0 += 32) {
     const int c = c0 + F.lane;
     bool valid = false;
-    uint64_t k = ~0ull;
+    uint32_t k = 0;
     if (c < C.Q) {
       valid = (c < C.n) ? ((F.sgnV[c] & 0xf) != 0) : ((F.sgnC[c - C.n] & PRESENT) != 0);
-      if (valid) {
-        float f = __double2float_rn(F.d2[c]);  // monotone non-decreasing map
-        uint32_t fb = __float_as_uint(f) & 0x7fffffffu;
-        k = ((uint64_t)(~fb) << 32) | (uint32_t)c;
-      }
+      if (valid) k = ~(__float_as_uint(__double2float_rn(F.d2[c])) & 0x7fffffffu);
     }
     const unsigned bal = __ballot_sync(FULL, valid);
-    if (valid) keys[nv + __popc(bal & lt)] = k;
+    if (valid) {
+      const int at = nv + __popc(bal & lt);
+      kA[at] = k;
+      cA[at] = (uint16_t)c;
+    }
     nv += __popc(bal);
   }
-  int N = 1;   // power of two >= #valid (<= QP2, the key array's length)
-  while (N < nv) N <<= 1;
-  for (int c = nv + F.lane; c < C.QP2; c += 32) keys[c] = ~0ull;
   __syncwarp();
-  // Bitonic network; each lane's compare-exchanges of a stage are independent, so they are
-  // done four at a time with all eight loads issued before any store (latency overlap).
-  for (int k = 2; k <= N; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t0 = F.lane; t0 < (N >> 1); t0 += 128) {
-        int lo[4], hi[4];
-        uint64_t a[4], b[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int t = t0 + 32 * u;
-          lo[u] = ((t & ~(j - 1)) << 1) | (t & (j - 1));   // 2 j (t / j) + t % j, j = 2^k
-          hi[u] = lo[u] + j;
-          const bool ok = t < (N >> 1);
-          a[u] = ok ? keys[lo[u]] : 0ull;
-          b[u] = ok ? keys[hi[u]] : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int t = t0 + 32 * u;
-          const bool up = ((lo[u] & k) == 0);
-          if (t < (N >> 1) && (a[u] > b[u]) == up) {
-            keys[lo[u]] = b[u];
-            keys[hi[u]] = a[u];
-          }
-        }
-      }
+  uint32_t* ks = kA;
+  uint32_t* kd = kB;
+  uint16_t* cs = cA;
+  uint16_t* cd = cB;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 8 * pass;
+    for (int b = F.lane; b < 256; b += 32) hist[b] = 0u;
+    __syncwarp();
+    for (int c0 = 0; c0 < nv; c0 += 32) {
+      const int c = c0 + F.lane;
+      const int dg = (c < nv) ? (int)((ks[c] >> sh) & 0xffu) : -1 - F.lane;
+      const unsigned peers = __match_any_sync(FULL, dg);
+      if (c < nv && (__ffs(peers) - 1) == F.lane) hist[dg] += (uint32_t)__popc(peers);
       __syncwarp();
     }
+    // exclusive scan of the 256 bins (8 consecutive bins per lane); skip a constant digit
+    uint32_t v[8], tot = 0;
+    bool single = false;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      v[t] = hist[8 * F.lane + t];
+      single |= (v[t] == (uint32_t)nv);
+      tot += v[t];
+    }
+    if (__any_sync(FULL, single)) continue;   // every key has the same digit: order unchanged
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (F.lane >= o) incl += y;
+    }
+    uint32_t run = incl - tot;
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      hist[8 * F.lane + t] = run;
+      run += v[t];
+    }
+    __syncwarp();
+    // stable scatter, 32 keys at a time in order: rank among equal digits by lane order
+    for (int c0 = 0; c0 < nv; c0 += 32) {
+      const int c = c0 + F.lane;
+      const bool ok = c < nv;
+      const uint32_t k = ok ? ks[c] : 0u;
+      const int dg = ok ? (int)((k >> sh) & 0xffu) : -1 - F.lane;
+      const unsigned peers = __match_any_sync(FULL, dg);
+      if (ok) {
+        const uint32_t at = hist[dg] + (uint32_t)__popc(peers & lt);
+        kd[at] = k;
+        cd[at] = cs[c];
+      }
+      __syncwarp();
+      if (ok && (__ffs(peers) - 1) == F.lane) hist[dg] += (uint32_t)__popc(peers);
+      __syncwarp();
+    }
+    uint32_t* tk = ks; ks = kd; kd = tk;
+    uint16_t* tc = cs; cs = cd; cd = tc;
   }
+  for (int r = F.lane; r < C.Q; r += 32) order[r] = (r < nv) ? cs[r] : NONE16;
+  __syncwarp();
   // Equal float keys are ordered by column; that is the exact (fp64 weight desc, column asc)
   // order unless some adjacent pair inside a float tie has a strictly smaller exact weight
   // first.  Checked in parallel; only then does the serial fix-up below run (e.g. never at
   // IPM iteration 0, where every weight is exactly 1).
   bool tie = false;
-  for (int r = F.lane; r + 1 < nv; r += 32) {
-    uint64_t a = keys[r], b = keys[r + 1];
-    if ((a >> 32) == (b >> 32)) {
-      const double wa = F.d2[(int)(a & 0xffffffffu)], wb = F.d2[(int)(b & 0xffffffffu)];
-      if (wa < wb) tie = true;
-    }
-  }
+  for (int r = F.lane; r + 1 < nv; r += 32)
+    if (ks[r] == ks[r + 1] && F.d2[order[r]] < F.d2[order[r + 1]]) tie = true;
   if (__any_sync(FULL, tie)) {
     if (F.lane == 0) {
       int r = 0;
-      while (r + 1 < C.Q && keys[r] != ~0ull) {
-        uint64_t hi32 = keys[r] >> 32;
+      while (r + 1 < nv) {
+        const uint32_t key = ks[r];
         int e = r + 1;
-        while (e < C.Q && keys[e] != ~0ull && (keys[e] >> 32) == hi32) ++e;
-        for (int a = r + 1; a < e; ++a) {  // insertion sort by (d2 desc, column asc)
-          uint64_t ka = keys[a];
-          int ca = (int)(ka & 0xffffffffu);
-          double wa = F.d2[ca];
+        while (e < nv && ks[e] == key) ++e;
+        for (int a = r + 1; a < e; ++a) {   // insertion sort by (d2 desc, column asc)
+          const uint16_t ca = order[a];
+          const double wa = F.d2[ca];
           int b = a - 1;
           while (b >= r) {
-            int cb = (int)(keys[b] & 0xffffffffu);
-            double wb = F.d2[cb];
+            const uint16_t cb = order[b];
+            const double wb = F.d2[cb];
             if (!((wa > wb) || (wa == wb && ca < cb))) break;
-            keys[b + 1] = keys[b];
+            order[b + 1] = cb;
             --b;
           }
-          keys[b + 1] = ka;
+          order[b + 1] = ca;
         }
         r = e;
       }
     }
     __syncwarp();
   }
+  return nv;
 }
 
-// Part 2: Alg. 7 (P:662-678).  DEG1 (line 4) is a bitmap over ranks; line 6 = first set bit.
-// For each column: number of live rows and XOR of their ids (the unique live row of a
-// degree-1 column).  Pick k records pos[R] = k, pcol[R] = c, prow[k] = R (line 7) and
-// zeroes row R (line 8), updating degrees and DEG1 (line 9).
-__device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
+// Alg. 7 lines 5-9, the p picks.  DEG1 as a rank bitmap: bit r set <=> the column of rank r
+// currently has exactly one live row; "the maximum-weight column in DEG1" (line 6) is the
+// first set bit.  Pick k: r -> column c = order[r] -> its live row R = xr[c] (XOR of live
+// rows); record it (line 7); kill row R (line 8): the <= d_c + 1 columns of R lose a live row,
+// entering DEG1 at degree 1 and leaving it at degree 0 (line 9).
+// Register variant: lane l owns bitmap words l, 32 + l, ... (K per lane), so the search is a
+// ballot and the updates are shuffles — no shared-memory atomics on the pick's critical path.
+template <int K>
+__device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint16_t* order,
+                                               const uint16_t* rank, uint8_t* cnt, uint16_t* xr,
+                                               const unsigned long long* bm, uint16_t* pos,
+                                               uint16_t* pcol, uint16_t* prow) {
   const DCode& C = *F.C;
-  const Layout& L = *F.L;
-  uint64_t* keys = F.S<uint64_t>(L.s_keys);
-  uint16_t* order = F.S<uint16_t>(L.s_order);
-  uint16_t* rank = F.S<uint16_t>(L.s_rank);
-  uint8_t* cnt = F.S<uint8_t>(L.s_cnt);
-  uint16_t* xr = F.S<uint16_t>(L.s_xr);
-  unsigned long long* bm = F.S<unsigned long long>(L.s_bm);
-  uint16_t* pos = F.S<uint16_t>(L.s_pos);
-  uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
-  uint16_t* prow = F.S<uint16_t>(L.s_prow);
-  // in-place extraction of the sorted order (chunked: a lane never overwrites an unread key)
-  for (int base = 0; base < C.Q; base += 32) {
-    int r = base + F.lane;
-    uint16_t o = NONE16;
-    if (r < C.Q) {
-      uint64_t k = keys[r];
-      o = (k == ~0ull) ? NONE16 : (uint16_t)(k & 0xffffu);
+  unsigned long long wd[K];
+#pragma unroll
+  for (int kk = 0; kk < K; ++kk) {
+    const int w = 32 * kk + F.lane;
+    wd[kk] = (w < C.W) ? bm[w] : 0ull;
+  }
+  for (int k = 0; k < p; ++k) {
+    int r = 0;
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const unsigned bal = __ballot_sync(FULL, wd[kk] != 0ull);
+      if (bal) {
+        const int src = __ffs(bal) - 1;
+        const unsigned long long w0 = __shfl_sync(FULL, wd[kk], src);
+        r = (32 * kk + src) * 64 + (__ffsll((long long)w0) - 1);
+        break;
+      }
+    }
+    const int c = order[r];
+    const int R = xr[c];
+    if (F.lane == 0) {
+      pos[R] = (uint16_t)k;
+      pcol[R] = (uint16_t)c;
+      prow[k] = (uint16_t)R;
+    }
+    const int deg = C.chk_deg[R];
+    int upd = -1;   // rank << 1 | set (degree 1) ; -1: no DEG1 change
+    if (F.lane <= deg) {
+      const int cc = (F.lane < deg) ? chk_nb(C, R, F.lane) : (C.n + R);
+      const int nc = (int)cnt[cc] - 1;
+      cnt[cc] = (uint8_t)nc;
+      xr[cc] = (uint16_t)(xr[cc] ^ R);
+      if (nc <= 1) upd = ((int)rank[cc] << 1) | (nc == 1 ? 1 : 0);
+    }
+    // apply the (<= d_c + 1) bit updates in the owning lanes
+    for (int t = 0; t <= deg; ++t) {
+      const int u = __shfl_sync(FULL, upd, t);
+      if (u < 0) continue;
+      const int rr = u >> 1;
+      const int wi = rr >> 6;
+      if ((wi & 31) == F.lane) {
+        const unsigned long long bit = 1ull << (rr & 63);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+          if ((wi >> 5) == kk) wd[kk] = (u & 1) ? (wd[kk] | bit) : (wd[kk] & ~bit);
+      }
     }
     __syncwarp();
-    if (r < C.Q) order[r] = o;
-    __syncwarp();
   }
-  for (int c = F.lane; c < C.Q; c += 32) rank[c] = NONE16;
-  for (int w = F.lane; w < C.W; w += 32) bm[w] = 0ull;
-  __syncwarp();
-  for (int r = F.lane; r < C.Q; r += 32) {
-    uint16_t c = order[r];
-    if (c != NONE16) rank[c] = (uint16_t)r;
-  }
-  __syncwarp();
-  for (int c = F.lane; c < C.Q; c += 32) {
-    int cn = 0, x = 0;
-    if (c < C.n) {
-      uint8_t s = F.sgnV[c];
-      int dv = C.var_deg[c];
-      for (int k = 0; k < dv; ++k)
-        if ((s >> k) & 1) {
-          ++cn;
-          x ^= var_ck(C, c, k);
-        }
-    } else if (F.sgnC[c - C.n] & PRESENT) {
-      cn = 1;
-      x = c - C.n;
-    }
-    cnt[c] = (uint8_t)cn;
-    xr[c] = (uint16_t)x;
-    if (cn == 1) {
-      int r = rank[c];
-      atomicOr(&bm[r >> 6], 1ull << (r & 63));
-    }
-  }
-  __syncwarp();
+}
+
+// Shared-memory variant for large codes (W > 128 words).
+__device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16_t* order,
+                                             const uint16_t* rank, uint8_t* cnt, uint16_t* xr,
+                                             unsigned long long* bm, uint16_t* pos, uint16_t* pcol,
+                                             uint16_t* prow) {
+  const DCode& C = *F.C;
   for (int k = 0; k < p; ++k) {
     int r = 0;
     for (int base = 0; base < C.W; base += 32) {
@@ -516,6 +563,57 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
     }
     __syncwarp();
   }
+}
+
+// Part 2: Alg. 7 (P:662-678).  DEG1 (line 4) is a bitmap over ranks; line 6 = first set bit.
+// For each column: number of live rows and XOR of their ids (the unique live row of a
+// degree-1 column).  Pick k records pos[R] = k, pcol[R] = c, prow[k] = R (line 7) and
+// zeroes row R (line 8), updating degrees and DEG1 (line 9).
+__device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
+  const DCode& C = *F.C;
+  const Layout& L = *F.L;
+  uint16_t* order = F.S<uint16_t>(L.s_order);
+  uint16_t* rank = F.S<uint16_t>(L.s_rank);
+  uint8_t* cnt = F.S<uint8_t>(L.s_cnt);
+  uint16_t* xr = F.S<uint16_t>(L.s_xr);
+  unsigned long long* bm = F.S<unsigned long long>(L.s_bm);
+  uint16_t* pos = F.S<uint16_t>(L.s_pos);
+  uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
+  uint16_t* prow = F.S<uint16_t>(L.s_prow);
+  for (int c = F.lane; c < C.Q; c += 32) rank[c] = NONE16;
+  for (int w = F.lane; w < C.W; w += 32) bm[w] = 0ull;
+  __syncwarp();
+  for (int r = F.lane; r < C.Q; r += 32) {
+    uint16_t c = order[r];
+    if (c != NONE16) rank[c] = (uint16_t)r;
+  }
+  __syncwarp();
+  for (int c = F.lane; c < C.Q; c += 32) {
+    int cn = 0, x = 0;
+    if (c < C.n) {
+      uint8_t s = F.sgnV[c];
+      int dv = C.var_deg[c];
+      for (int k = 0; k < dv; ++k)
+        if ((s >> k) & 1) {
+          ++cn;
+          x ^= var_ck(C, c, k);
+        }
+    } else if (F.sgnC[c - C.n] & PRESENT) {
+      cn = 1;
+      x = c - C.n;
+    }
+    cnt[c] = (uint8_t)cn;
+    xr[c] = (uint16_t)x;
+    if (cn == 1) {
+      int r = rank[c];
+      atomicOr(&bm[r >> 6], 1ull << (r & 63));
+    }
+  }
+  __syncwarp();
+  if (C.W <= 32) peel_picks_reg<1>(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
+  else if (C.W <= 64) peel_picks_reg<2>(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
+  else if (C.W <= 128) peel_picks_reg<4>(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
+  else peel_picks_smem(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
 }
 
 // Sweep dependencies of the pivot on row R (A_M is upper triangular in pick order):
@@ -1012,13 +1110,73 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
   return ABS ? 0.0 : wsum(hl);
 }
 
+constexpr int PCG_REFINE_MAX = 6;
+
+// double-double helpers (Knuth two-sum, fma two-product)
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, double b) {
+  const double s = a.hi + b;
+  const double bb = s - a.hi;
+  const double e = (a.hi - (s - bb)) + (b - bb) + a.lo;
+  const double h = s + e;
+  return DD{h, e - (h - s)};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD t = dd_add(a, b.hi);
+  return dd_add(t, b.lo);
+}
+__device__ __forceinline__ DD dd_mul(DD a, double b) {
+  const double p = a.hi * b;
+  const double e = fma(a.hi, b, -p) + a.lo * b;
+  const double h = p + e;
+  return DD{h, e - (h - p)};
+}
+
+// r = w - Q dy in double-double (Q = A D^2 A^T applied matrix-free, one pass over the checks,
+// (A^T dy)_i recomputed per edge); rounded r to rS, returns ||r||^2.  The residual itself is then
+// accurate far below the fp64 evaluation floor, which is what lets refinement converge.
+__device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
+  const DCode& C = *F.C;
+  double acc = 0.0;
+  for (int j = F.lane; j < C.m; j += 32) {
+    const uint16_t sc = F.sgnC[j];
+    double r = 0.0;
+    if (sc & PRESENT) {
+      DD l = dd_mul(DD{F.dy[j], 0.0}, F.d2[C.n + j]);
+      const int deg = C.chk_deg[j];
+      for (int t = 0; t < deg; ++t) {
+        const int i = chk_nb(C, j, t);
+        const uint8_t sv = F.sgnV[i];
+        DD ti{0.0, 0.0};
+        for (int k = 0; k < C.var_deg[i]; ++k) {
+          if (!((sv >> k) & 1)) continue;
+          const double h = F.dy[var_ck(C, i, k)];
+          ti = dd_add(ti, ((sv >> (4 + k)) & 1) ? -h : h);
+        }
+        DD ui = dd_mul(ti, F.d2[i]);
+        if ((sc >> t) & 1) ui = DD{-ui.hi, -ui.lo};
+        l = dd_add(l, ui);
+      }
+      const DD rr = dd_add(DD{-l.hi, -l.lo}, F.w[j]);
+      r = rr.hi + rr.lo;
+    }
+    rS[j] = r;
+    acc += r * r;
+  }
+  __syncwarp();
+  return wsum(acc);
+}
+
 // PCG (Alg. 4) from dy = 0, r = w, in preconditioner mode `mode`.  The recursion
 // stops after line 9 once ||r||_2 <= itol ||w||_2 (G15, C-9; itol <= pcg_rel_tol is the
 // inexact-Newton target of the caller); once ||r|| <= pcg_rel_tol ||w|| (the acceptance test of
 // C-9) the recursion gets at most 50 more iterations towards itol.  It also ends at the cap, on a
 // breakdown (h^T Q h or z^T r not > 0 / non-finite; both are sums of squares, so only 0 / inf /
-// nan), or on a stall (no new minimum of ||r|| in 200 iterations for MTS, 1000 for CG, or
-// 1e8-fold growth; R-1).  The TRUE residual w - Q dy is then evaluated once.
+// nan), or on divergence (||r|| 1e8-fold above its minimum).  There is no early stall exit:
+// late-IPM systems of fractional LPs often make no progress for a few hundred
+// iterations and then converge, and cutting them short stalls the IPM (measured, R-1).  The TRUE residual w - Q dy is then evaluated once.
 // `refine` (ipm_step_pcg only): while the true residual fails pcg_rel_tol, restart from it
 // (iterative refinement with the same preconditioner, at most 4 restarts); a restart that no
 // longer halves it within 1e3x of the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||
@@ -1048,11 +1206,11 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
   PcgResult res{0, 0, 0.0, 0.0};
   if (wn == 0.0) return res;
   const double tol = P.pcg_rel_tol * wn;                       // acceptance (C-9)
-  const double itol = fmin(itol_rel, P.pcg_rel_tol) * wn;      // recursion target
+  double itol = fmin(itol_rel, P.pcg_rel_tol) * wn;            // recursion target
   const int cap = P.pcg_max_iter;
   int it = 0;
   double prev_trn = 1e308;
-  for (int restart = 0; restart <= (refine ? 4 : 0); ++restart) {
+  for (int restart = 0; restart <= (refine ? PCG_REFINE_MAX : 0); ++restart) {
     double rz;
     precond_apply(F, mode, nLb, nLf, rz);   // line 3
     if (!(rz > 0.0) || !isfinite(rz)) {
@@ -1105,7 +1263,7 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
       if (rr < rrmin) {
         rrmin = rr;
         since_min = 0;
-      } else if (rr > 1e16 * rrmin || ++since_min > (mode == PC_MTS ? 200 : 1000)) {
+      } else if (rr > 1e16 * rrmin || ++since_min > 1000) {
         st = (rrmin <= tol * tol) ? 0 : ST_PCG_MAXITER;   // stall
         break;
       }
@@ -1129,35 +1287,53 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
     ALP_TICK(F, CY_PCG, tk);
     res.rec_relres = sqrt(rr) / wn;
     if (st == 0 && !(res.rec_relres <= P.pcg_rel_tol)) st = ST_PCG_MAXITER;
-    // TRUE residual r = w - Q dy (h <- dy; h is rebuilt on a restart)
-    for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
-    __syncwarp();
-    spmv<false>(F);
-    double tr = 0.0;
-    for (int j = F.lane; j < C.m; j += 32) {
-      double r = 0.0;
-      if (F.sgnC[j] & PRESENT) r = F.w[j] - F.l[j];
-      rS[j] = r;
-      tr += r * r;
+    // TRUE residual r = w - Q dy: fp64 in the decode (reported), double-double in refine mode
+    // (ipm_step_pcg), where it drives the refinement restarts
+    double trn;
+    if (refine) {
+      trn = sqrt(residual_dd(F, rS));
+    } else {
+      for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
+      __syncwarp();
+      spmv<false>(F);
+      double tr = 0.0;
+      for (int j = F.lane; j < C.m; j += 32) {
+        double r = 0.0;
+        if (F.sgnC[j] & PRESENT) r = F.w[j] - F.l[j];
+        rS[j] = r;
+        tr += r * r;
+      }
+      __syncwarp();
+      trn = sqrt(wsum(tr));
     }
-    __syncwarp();
-    const double trn = sqrt(wsum(tr));
     res.relres = trn / wn;
     res.status = st;
     ALP_TICK(F, CY_PCG, tk);
     if (!refine || st == ST_PCG_BREAKDOWN || !isfinite(trn)) break;
-    if (trn <= tol) break;   // the true residual meets C-9
-    spmv<true>(F);           // attainable-accuracy floor of the residual evaluation itself
-    double aa = 0.0;
-    for (int j = F.lane; j < C.m; j += 32)
-      if (F.sgnC[j] & PRESENT) aa += F.l[j] * F.l[j];
-    const double floor_est = 16.0 * 2.220446049250313e-16 * sqrt(wsum(aa));
-    if (trn <= floor_est || (trn > 0.5 * prev_trn && trn <= 1e3 * floor_est)) {
-      res.status = (st == 0) ? ST_PCG_FLOOR : st;
+    // Iterative refinement with double-double residuals: restart PCG on Q delta = r (the same
+    // preconditioner), dy += delta, while the correction keeps shrinking: stop once
+    // ||delta|| <= 1e-13 ||dy||, or ||delta|| no longer halves, or after PCG_REFINE_MAX restarts.
+    // (The residual of a rounded fp64 dy cannot fall below ~eps || |A| D^2 |A|^T |dy| ||, so its
+    // norm is no stopping signal near the floor; the correction size is.)  Each restart aims
+    // 1e-6 below its starting residual.  PCG_FLOOR: the TRUE residual stayed above pcg_rel_tol.
+    double dn = 0.0, yn = 0.0;
+    if (restart > 0) {
+      for (int j = F.lane; j < C.m; j += 32) {
+        const double d = F.dy[j] - F.v[j];
+        dn += d * d;
+        yn += F.dy[j] * F.dy[j];
+      }
+      dn = sqrt(wsum(dn));
+      yn = sqrt(wsum(yn));
+    }
+    if (st != 0 || restart == PCG_REFINE_MAX || (restart > 0 && (dn <= 1e-13 * yn || dn > 0.5 * prev_trn))) {
+      if (st == 0 && trn > tol) res.status = ST_PCG_FLOOR;
       break;
     }
-    if (st != 0) break;     // the recursion itself failed: no refinement
-    prev_trn = trn;
+    if (restart > 0) prev_trn = dn;
+    for (int j = F.lane; j < C.m; j += 32) F.v[j] = F.dy[j];   // dy before the next correction
+    __syncwarp();
+    itol = 1e-6 * trn;
   }
   res.iters = it;
   return res;
