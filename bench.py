@@ -43,13 +43,26 @@ FRAMES_PER_RANK = 16384
 SNRS = [2.0, 2.5, 3.0]
 
 
+CONFIG_DESC = {
+    1: ("C1: random (3,6)-regular LDPC n=120 m=60", "rnd(3,6) n=120 m=60 seed 1001", [3.0], "all-zero codeword"),
+    2: ("C2: random (3,6)-regular LDPC n=1000 m=500", "rnd(3,6) n=1000 m=500 seed 1002", [2.0, 2.5, 3.0],
+        "random-codeword"),
+    3: ("C3: random (3,12)-regular LDPC n=4000 m=1000", "rnd(3,12) n=4000 m=1000 seed 1003", [3.5], "all-zero codeword"),
+    4: ("C4: random (3,6)-regular LDPC n=32000 m=16000", "rnd(3,6) n=32000 m=16000 seed 1004", [2.2],
+        "random-codeword"),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--snr-idx", type=int, default=2)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4],
+                    help="BASELINE.json config of the decode workload (2 = the metric's; 1/3/4 = the "
+                         "other decode configs, e.g. --config 4 --frames 1184 for the n=32,000 line)")
+    ap.add_argument("--snr-idx", type=int, default=None, help="Eb/N0 index (config 2: 0/1/2 = 2.0/2.5/3.0 dB)")
     ap.add_argument("--frames", type=int, default=FRAMES_PER_RANK, help="frames per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -58,7 +71,13 @@ def parse():
                     help="also decode the config's other SNRs (2.0, 2.5 dB) once each and report them")
     ap.add_argument("--step-systems", type=int, default=65536,
                     help="config-5 isolated step solves timed beside the decode (0 = skip)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.snr_idx is None:
+        a.snr_idx = 2 if a.config == 2 else 0
+    a.snrs = CONFIG_DESC[a.config][2]
+    if a.config != 2:
+        a.snr_sweep = 0
+    return a
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -70,16 +89,17 @@ def dist_env():
 
 
 def workload_config(args, ws):
+    desc, code_desc, snrs, kind = CONFIG_DESC[args.config]
     return {
-        "workload": f"C2: random (3,6)-regular LDPC n=1000 m=500, {args.frames} random-codeword "
-                    f"frames per GPU, BPSK/AWGN Eb/N0={SNRS[args.snr_idx]} dB, fp64 LLR, MALP-A + "
+        "workload": f"{desc}, {args.frames} {kind} "
+                    f"frames per GPU, BPSK/AWGN Eb/N0={snrs[args.snr_idx]} dB, fp64 LLR, MALP-A + "
                     "primal-dual IPM + PCG (column-wise MTS preconditioner) to recursive rel. "
                     "residual 1e-8 (forcing term min(1e-8, 1e-2 mu)) with the basis-corrected "
                     "Newton recovery (DESIGN.md C-32)",
-        "code": "rnd(3,6) n=1000 m=500 seed 1002",
+        "code": code_desc,
         "frames_per_gpu": args.frames,
         "global_frames": args.frames * ws,
-        "ebn0_db": SNRS[args.snr_idx],
+        "ebn0_db": snrs[args.snr_idx],
         "parallelism": f"frame-sharded dp{ws}",
         "l2": "256 MiB L2 flush between timed steps (LLR input 131 MB also exceeds L2)",
     }
@@ -153,18 +173,18 @@ def measured_peak_hbm():
 def _oracle_worker(args_tuple):
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)   # one BLAS thread per worker process
-    snr_idx, frames = args_tuple
+    cfg, snr_idx, frames = args_tuple
     from synth import config_code, config_frames
     from oracle.lp import malp_decode
-    code = config_code(2)
-    fb = config_frames(2, snr_idx, frames=frames, code=code)
+    code = config_code(cfg)
+    fb = config_frames(cfg, snr_idx, frames=frames, code=code)
     t0 = time.perf_counter()
     for f in range(fb.F):
         malp_decode(code, fb.llr[f])
     return fb.F, time.perf_counter() - t0
 
 
-def time_oracle(snr_idx: int, budget_s: float, frame_offset: int = 0):
+def time_oracle(snr_idx: int, budget_s: float, frame_offset: int = 0, cfg: int = 2):
     """Oracle MALP-A decode (fp64, dense Cholesky) on the host cores: one frame per worker
     process, frames taken in order from frame_offset, workers run until budget_s elapses.
     Returns (frames/s, cores, frames decoded)."""
@@ -180,7 +200,7 @@ def time_oracle(snr_idx: int, budget_s: float, frame_offset: int = 0):
     try:
         with ctx.Pool(cores) as pool:
             while True:
-                jobs = [(snr_idx, list(range(nxt + w * per, nxt + (w + 1) * per))) for w in range(cores)]
+                jobs = [(cfg, snr_idx, list(range(nxt + w * per, nxt + (w + 1) * per))) for w in range(cores)]
                 nxt += cores * per
                 for F, _ in pool.map(_oracle_worker, jobs):
                     done += F
@@ -203,7 +223,7 @@ def run_reference(args):
     times, frames = [], 0
     budget = max(2.0, min(args.cpu_seconds, 60.0))
     for s in range(args.warmup + args.steps):
-        fps, cores, nf, wall = time_oracle(args.snr_idx, budget / 2, frame_offset=0)
+        fps, cores, nf, wall = time_oracle(args.snr_idx, budget / 2, frame_offset=0, cfg=args.config)
         if s >= args.warmup:
             times.append(wall)
             frames += nf
@@ -238,10 +258,10 @@ def run_ours(args):
     from paper_0902_0657_b200.dist import shard_frame_ids, frame_counters, reduce_run, counters_dict
     from synth import config_code, config_frames
 
-    code = config_code(2)
+    code = config_code(args.config)
     # this rank's frames: global frame g = rank + ws * t (interleaved sharding)
     frame_ids = shard_frame_ids(args.frames, rank, ws)
-    fb = config_frames(2, args.snr_idx, frames=frame_ids, code=code)
+    fb = config_frames(args.config, args.snr_idx, frames=frame_ids, code=code)
     llr_host = torch.from_numpy(fb.llr).pin_memory()
     llr = llr_host.to(dev)
     c = alp.Code.from_synth(code)
@@ -373,8 +393,8 @@ def run_ours(args):
                                                       **counters_dict(cs))
     if args.step_systems > 0:
         line["step_solve"] = time_step_solve(args, dev, stream)
-    if ws == 1 and not args.no_cpu_baseline:
-        fps, cores, nf, wall = time_oracle(args.snr_idx, args.cpu_seconds)
+    if ws == 1 and not args.no_cpu_baseline and args.config != 4:
+        fps, cores, nf, wall = time_oracle(args.snr_idx, args.cpu_seconds, cfg=args.config)
         line["cpu_baseline"] = {
             "value": fps, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {nf} frames of the same workload, MALP-A oracle (fp64 numpy, dense "

@@ -59,7 +59,7 @@ typedef enum {
   ALP_ERR_INVALID_ARG = -1,  /* null pointer where required, negative size, bad params   */
   ALP_ERR_BAD_CODE = -2,     /* Tanner graph invalid: index out of range, duplicate, ... */
   ALP_ERR_UNSUPPORTED = -3,  /* valid but beyond this build: d_c > 15, d_v > 4,
-                                n + m > 65535, per-frame shared memory over the device limit */
+                                n + m > 65535, m > 32767                                      */
   ALP_ERR_CUDA = -4,         /* a CUDA call failed (no device, launch failure, fault)    */
   ALP_ERR_WORKSPACE = -5     /* workspace NULL, misaligned or smaller than required      */
 } alp_status;

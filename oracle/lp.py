@@ -167,30 +167,39 @@ def cholesky_solve(Q: np.ndarray, w: np.ndarray, info: dict | None = None) -> np
     return sla.solve_triangular(L.T, t, lower=False)
 
 
-def step_solve_exact(A, d2: np.ndarray, w: np.ndarray, refine: int = 4) -> np.ndarray:
+def step_solve_exact(A, d2: np.ndarray, w: np.ndarray, refine: int = 12) -> np.ndarray:
     """dy = Q^-1 w, Q = A D^2 A^T (eq.`Delta y`), to full fp64 accuracy even when
     kappa(Q) ~ 1e18 (config 5, d^2 over 24 decades; SURVEY C-27).
 
-    The plain definition computed in extended precision: Q is formed in numpy longdouble
-    (x87 80-bit, eps 1.1e-19; A is +-1/0 and d2 fp64, so the products are exact), factored
-    by a textbook column Cholesky in longdouble, and the solution is iteratively refined
-    with longdouble residuals w - Q dy (converges while kappa * 1e-19 < 1).  Reference for
-    the GPU PCG parity of ipm_step_pcg; fp64 Cholesky (cholesky_solve) cannot serve there
-    because its own forward error reaches kappa * eps."""
+    The plain definition, solved by iterative refinement whose residuals are EXACT: every input
+    is a dyadic rational (A is +-1/0, d2 and w are fp64), so r = w - A D^2 A^T y is computed in
+    exact rational arithmetic (fractions.Fraction over A's nonzeros), y itself is kept exact as
+    the sum of its corrections, and each correction solves Q delta = r with a long-double
+    (x87, eps 1.1e-19) column Cholesky of Q.  The error contracts by ~kappa * eps_longdouble per
+    step, so for kappa < ~1e18 the result is the correctly rounded solution after a few steps
+    (stop when a correction is below 1e-22 of |y|, at most `refine` steps).  (Refining with
+    long-double residuals alone, as round 1 did, stalls at kappa * eps_longdouble, ~1e-7 on some
+    config-5 systems — measured against this.)  Reference for the GPU PCG parity of
+    ipm_step_pcg; fp64 Cholesky (cholesky_solve) cannot serve there."""
+    from fractions import Fraction
     A = np.asarray(A.todense()) if sp.issparse(A) else np.asarray(A)
     ld = np.longdouble
     p = A.shape[0]
+    if p == 0:
+        return np.zeros(0)
+    d2 = np.asarray(d2, dtype=np.float64)
     # Q = sum_i d2_i a_i a_i^T over the columns a_i of A (the definition, summed column by
-    # column; A is +-1/0 so each term is exact in longdouble) — only the nonzeros of a_i touch Q
+    # column) — only the nonzeros of a_i touch Q
     Q = np.zeros((p, p), dtype=ld)
-    d2l = np.asarray(d2, dtype=np.float64).astype(ld)
+    d2l = d2.astype(ld)
+    cols = []
     for i in range(A.shape[1]):
         nz = np.nonzero(A[:, i])[0]
         if nz.size:
-            a = A[nz, i].astype(ld)
-            Q[np.ix_(nz, nz)] += d2l[i] * np.outer(a, a)
-    if p == 0:
-        return np.zeros(0)
+            a = A[nz, i]
+            cols.append((i, nz.tolist(), [int(v) for v in a]))
+            al = a.astype(ld)
+            Q[np.ix_(nz, nz)] += d2l[i] * np.outer(al, al)
     L = np.zeros_like(Q)
     for k in range(p):
         dkk = Q[k, k] - L[k, :k] @ L[k, :k]
@@ -208,11 +217,34 @@ def step_solve_exact(A, d2: np.ndarray, w: np.ndarray, refine: int = 4) -> np.nd
             y[k] = (t[k] - L[k + 1:, k] @ y[k + 1:]) / L[k, k]
         return y
 
-    wl = np.asarray(w, dtype=np.float64).astype(ld)
-    y = solve(wl)
+    def exact(v):   # a long double as an exact rational (its fp64 head + fp64 tail)
+        h = float(v)
+        return Fraction(h) + Fraction(float(v - ld(h)))
+
+    d2f = [Fraction(float(v)) for v in d2]
+    wf = [Fraction(float(v)) for v in np.asarray(w, dtype=np.float64)]
+
+    def residual(yf):   # w - A (D^2 (A^T y)), exact
+        l = [Fraction(0)] * p
+        for i, nz, a in cols:
+            t = Fraction(0)
+            for r, av in zip(nz, a):
+                t = t + yf[r] if av > 0 else t - yf[r]
+            t *= d2f[i]
+            for r, av in zip(nz, a):
+                l[r] = l[r] + t if av > 0 else l[r] - t
+        return [wf[r] - l[r] for r in range(p)]
+
+    y = solve(np.asarray(w, dtype=np.float64).astype(ld))
+    yf = [exact(v) for v in y]
+    ynorm = float(np.linalg.norm(y.astype(np.float64)))
     for _ in range(refine):
-        y = y + solve(wl - Q @ y)
-    return y.astype(np.float64)
+        r = residual(yf)
+        dl = solve(np.array([float(v) for v in r], dtype=np.float64).astype(ld))
+        yf = [a + exact(b) for a, b in zip(yf, dl)]
+        if not float(np.linalg.norm(dl.astype(np.float64))) > 1e-22 * ynorm:
+            break
+    return np.array([float(v) for v in yf])
 
 
 def normal_matrix(A, d2: np.ndarray) -> np.ndarray:

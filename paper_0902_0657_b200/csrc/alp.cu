@@ -581,7 +581,7 @@ DCode make_dcode(const alp_code* c) {
   C.dv = c->dv;
   C.Q = c->n + c->m;
   C.W = (C.Q + 63) / 64;
-  C.RB = (int)al(1 + c->dc, 4);
+  C.RB = (c->dc + 1 <= 8) ? 8 : 16;   // back-record u16 words: head + <= d_c - 1 deps
   C.chk_var = c->d_chk_var;
   C.chk_deg = c->d_chk_deg;
   C.var_chk = c->d_var_chk;
@@ -611,8 +611,8 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.g_u = g(8 * n);
   L.g_b = g(8 * m);
   L.g_dinvF = g(8 * m);
-  L.g_recB = g(4 * m * C.RB);
-  L.g_recF = g(4 * m * RF);
+  L.g_recB = g(2 * m * C.RB);
+  L.g_recF = g(2 * m * RF);
   L.g_offB = g(4 * (m + 2));
   L.g_offF = g(4 * (m + 2));
   L.g_sgnC = g(2 * m);
@@ -636,12 +636,14 @@ Layout make_layout(const DCode& C, int smem_budget) {
   const size_t sort_base = a;
   L.s_sortk = (int)sort_base;
   L.s_sorth = (int)(sort_base + al(12 * Q, 16));
-  const size_t s_sort = sort_base + al(12 * Q, 16) + 1024;
+  const size_t s_sort = sort_base + al(12 * Q, 16) + 2048;
   a = sort_base;
   L.s_rank = s(2 * Q);
   L.s_cnt = s(Q);
   L.s_xr = s(2 * Q);
   L.s_bm = s(8 * (size_t)C.W);
+  L.RS = (C.dc + 1 <= 8) ? 8 : 16;
+  L.s_rrank = s(2 * (size_t)m * L.RS);
   L.s_pos = s(2 * m);
   L.s_pcol = s(2 * m);
   L.s_prow = s(2 * m);
@@ -675,7 +677,7 @@ Layout make_layout(const DCode& C, int smem_budget) {
   size_t tot = al(std::max(s_sort, std::max(end_peel, end_pcg)), 16);
   L.win_global = 0;
   L.g_win = 0;
-  if ((long long)tot > (long long)smem_budget) {
+  if ((long long)tot > 200 * 1024) {
     // large code: the whole phase window goes to the slot (global memory, L2-cached), nothing
     // is relocated, and the kernel needs no per-frame shared memory
     L.win_global = 1;
@@ -696,8 +698,8 @@ Layout make_layout(const DCode& C, int smem_budget) {
   rel_bytes[RL_DINVF] = 8 * m;
   rel_bytes[RL_OFFB] = 4 * (m + 2);
   rel_bytes[RL_OFFF] = 4 * (m + 2);
-  rel_bytes[RL_RECF] = 4 * m * (size_t)RF;
-  rel_bytes[RL_RECB] = 4 * m * (size_t)C.RB;
+  rel_bytes[RL_RECF] = 2 * m * (size_t)RF;
+  rel_bytes[RL_RECB] = 2 * m * (size_t)C.RB;
   rel_bytes[RL_D2] = 8 * Q;
   rel_bytes[RL_W] = 8 * m;
   for (int k = 0; k < RL_N; ++k) {
@@ -920,6 +922,7 @@ alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const i
   if (dc > DCMAX) return fail(ALP_ERR_UNSUPPORTED, "check degree > 15");
   if (dv > DVMAX) return fail(ALP_ERR_UNSUPPORTED, "variable degree > 4");
   if ((long long)n + m > 65535) return fail(ALP_ERR_UNSUPPORTED, "n + m > 65535");
+  if (m > 32767) return fail(ALP_ERR_UNSUPPORTED, "m > 32767 (15-bit row ids in the sweep records)");
   if (dv == 0) dv = 1;
   std::vector<uint16_t> chk_var((size_t)m * dc, 0xffff), var_chk((size_t)n * dv, 0xffff);
   std::vector<uint8_t> chk_deg(m), var_slot((size_t)n * dv, 0), var_deg(n, 0);

@@ -27,7 +27,8 @@ constexpr uint16_t PRESENT = 0x8000u;
 constexpr uint16_t NONE16 = 0xffffu;
 constexpr int DCMAX = 15;  // d_c <= 15 (mask bits 0..14)
 constexpr int DVMAX = 4;   // d_v <= 4  (sgnV packing: 4 present bits + 4 sign bits)
-constexpr int RF = 4;      // forward-record ints: head + up to d_v - 1 deps
+constexpr int RF = 4;      // forward-record u16: head + up to d_v - 1 deps (8 bytes)
+constexpr uint16_t NODEP = 0xffffu;   // unused dependency slot of a sweep record
 
 // frame status bits (include/alp.h alp_frame_status)
 constexpr int ST_ALP_MAXITER = 1, ST_IPM_MAXITER = 2, ST_PCG_MAXITER = 4, ST_PCG_BREAKDOWN = 8,
@@ -42,7 +43,7 @@ struct Params {
 
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
 struct DCode {
-  int n, m, dc, dv, Q, W, RB;             // Q = n + m columns, W = bitmap words
+  int n, m, dc, dv, Q, W, RB;             // Q = n + m columns, W = bitmap words, RB = back-record u16 (8/16)
   const uint16_t* __restrict__ chk_var;   // [m][dc] sorted variables of each check, 0xffff padded
   const uint8_t* __restrict__ chk_deg;    // [m]
   const uint16_t* __restrict__ var_chk;   // [n][dv] checks of each variable, 0xffff padded
@@ -93,6 +94,7 @@ struct Layout {
   int soff[12];
   int s_sortk, s_sorth;                                                        // sort phase
   int s_order, s_rank, s_cnt, s_xr, s_bm, s_pos, s_pcol, s_prow, s_lvB, s_lvF;  // peel phase
+  int s_rrank, RS;                      // peel: ranks of each row's columns, RS per row
   int s_poc, s_hist, s_cur;                                                    // post-peel
   int s_h, s_r, s_f, s_z, s_t;                                                 // PCG phase
 };
@@ -143,7 +145,8 @@ struct Frame {
   char* sm;
   double *x, *z, *d2, *v, *y, *dy, *l, *w, *u, *b, *dinvF, *rb, *rc;
   uint16_t* pcolR;  // [m]: pivot column of pivot row R (0..n+m-1), NONE16 if R is not a pivot
-  int *recB, *recF, *offB, *offF;
+  uint16_t *recB, *recF;  // sweep programs (u16 records, see build_precond)
+  int *offB, *offF;
   uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
   uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
   unsigned long long* hist;  // [alp_max_iter + 1] pool hashes of the LPs solved (C-12)
@@ -179,8 +182,8 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.u = (double*)(slot + L->g_u);
   F.b = (double*)(slot + L->g_b);
   F.dinvF = (double*)(slot + L->g_dinvF);
-  F.recB = (int*)(slot + L->g_recB);
-  F.recF = (int*)(slot + L->g_recF);
+  F.recB = (uint16_t*)(slot + L->g_recB);
+  F.recF = (uint16_t*)(slot + L->g_recF);
   F.offB = (int*)(slot + L->g_offB);
   F.offF = (int*)(slot + L->g_offF);
   F.sgnC = (uint16_t*)(slot + L->g_sgnC);
@@ -189,8 +192,8 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.rb = (double*)(slot + L->g_rb);
   F.rc = (double*)(slot + L->g_rc);
   F.pcolR = (uint16_t*)(slot + L->g_pcol);
-  F.recB = (int*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
-  F.recF = (int*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
+  F.recB = (uint16_t*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
+  F.recF = (uint16_t*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
   F.offB = (int*)rel_ptr(L, slot, sm, RL_OFFB, L->g_offB);
   F.offF = (int*)rel_ptr(L, slot, sm, RL_OFFF, L->g_offF);
   F.dinvF = (double*)rel_ptr(L, slot, sm, RL_DINVF, L->g_dinvF);
@@ -332,21 +335,24 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
 // weight d_i" among DEG1; weight d^2 = x/z gives the same order, C-10).
 // Valid columns (>= 1 present row; degree 0 in the extended Tanner graph otherwise) are
 // compacted in ascending column order with the 32-bit key ~bits(float(d^2)) (ascending key =
-// descending weight), then a stable LSD radix sort (4 passes of 8 bits, passes whose digit is
-// the same for every key skipped) orders them: descending float weight, ascending column on
-// equal floats.  Runs of equal float keys are then re-ordered by the exact fp64 weight (ties
+// descending weight), then a stable LSD radix sort (8 passes of 4 bits, per-lane contiguous
+// chunks, passes whose digit is the same for every key skipped) orders them: descending float
+// weight, ascending column on equal floats.  Runs of equal float keys are then re-ordered by the exact fp64 weight (ties
 // -> lower column).  Result: order[r] = column of rank r (r < nv), returns nv.
-// Buffers (shared window, sort phase): kA/kB u32[Q], cA/cB u16[Q], hist u32[256]; order
+// Buffers (shared window, sort phase): kA/kB u32[Q], cA/cB u16[Q], offs u32[16][32]; order
 // u16[Q] must not overlap them (layout: s_order, then s_sortk).
 // =====================================================================================
 __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
+  const uint16_t* __restrict__ sgnC = F.sgnC;
+  const uint8_t* __restrict__ sgnV = F.sgnV;
+  const double* __restrict__ d2 = F.d2;
   uint32_t* kA = F.S<uint32_t>(L.s_sortk);
   uint32_t* kB = kA + C.Q;
   uint16_t* cA = reinterpret_cast<uint16_t*>(kB + C.Q);
   uint16_t* cB = cA + C.Q;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(F.sm + L.s_sorth);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(F.sm + L.s_sorth);   // [16 digits][32 lanes]
   uint16_t* order = F.S<uint16_t>(L.s_order);
   const unsigned lt = (1u << F.lane) - 1u;
   int nv = 0;
@@ -355,8 +361,8 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
     bool valid = false;
     uint32_t k = 0;
     if (c < C.Q) {
-      valid = (c < C.n) ? ((F.sgnV[c] & 0xf) != 0) : ((F.sgnC[c - C.n] & PRESENT) != 0);
-      if (valid) k = ~(__float_as_uint(__double2float_rn(F.d2[c])) & 0x7fffffffu);
+      valid = (c < C.n) ? ((sgnV[c] & 0xf) != 0) : ((sgnC[c - C.n] & PRESENT) != 0);
+      if (valid) k = ~(__float_as_uint(__double2float_rn(d2[c])) & 0x7fffffffu);
     }
     const unsigned bal = __ballot_sync(FULL, valid);
     if (valid) {
@@ -367,61 +373,59 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
     nv += __popc(bal);
   }
   __syncwarp();
+  // LSD radix sort, 8 passes of 4-bit digits.  Lane l owns the contiguous chunk
+  // [l*ch, (l+1)*ch) of the current sequence, so lane order = sequence order and the scatter
+  // (digit base + earlier lanes' counts + this lane's running count) is stable.  Per-lane digit
+  // counts live in registers (four packed u64, 16 bits per digit: ch <= 65535).
+  const int ch = (nv + 31) >> 5;
+  const int lo = min(nv, F.lane * ch), hi = min(nv, lo + ch);
   uint32_t* ks = kA;
   uint32_t* kd = kB;
   uint16_t* cs = cA;
   uint16_t* cd = cB;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int sh = 8 * pass;
-    for (int b = F.lane; b < 256; b += 32) hist[b] = 0u;
-    __syncwarp();
-    for (int c0 = 0; c0 < nv; c0 += 32) {
-      const int c = c0 + F.lane;
-      const int dg = (c < nv) ? (int)((ks[c] >> sh) & 0xffu) : -1 - F.lane;
-      const unsigned peers = __match_any_sync(FULL, dg);
-      if (c < nv && (__ffs(peers) - 1) == F.lane) hist[dg] += (uint32_t)__popc(peers);
-      __syncwarp();
+  for (int sh = 0; sh < 32; sh += 4) {
+    unsigned long long q0 = 0ull, q1 = 0ull, q2 = 0ull, q3 = 0ull;
+    for (int i = lo; i < hi; ++i) {
+      const int dg = (ks[i] >> sh) & 0xf;
+      const unsigned long long inc = 1ull << (16 * (dg & 3));
+      const int w = dg >> 2;
+      q0 += (w == 0) ? inc : 0ull;
+      q1 += (w == 1) ? inc : 0ull;
+      q2 += (w == 2) ? inc : 0ull;
+      q3 += (w == 3) ? inc : 0ull;
     }
-    // exclusive scan of the 256 bins (8 consecutive bins per lane); skip a constant digit
-    uint32_t v[8], tot = 0;
-    bool single = false;
+    // exclusive offsets per (digit, lane); a pass whose digit is the same for every key is skipped
+    int base = 0;
+    bool skip = false;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      v[t] = hist[8 * F.lane + t];
-      single |= (v[t] == (uint32_t)nv);
-      tot += v[t];
-    }
-    if (__any_sync(FULL, single)) continue;   // every key has the same digit: order unchanged
-    uint32_t incl = tot;
+    for (int dg = 0; dg < 16; ++dg) {
+      const unsigned long long qw = (dg < 4) ? q0 : (dg < 8) ? q1 : (dg < 12) ? q2 : q3;
+      const int cnt = (int)((qw >> (16 * (dg & 3))) & 0xffffull);
+      int incl = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, incl, o);
-      if (F.lane >= o) incl += y;
-    }
-    uint32_t run = incl - tot;
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      hist[8 * F.lane + t] = run;
-      run += v[t];
-    }
-    __syncwarp();
-    // stable scatter, 32 keys at a time in order: rank among equal digits by lane order
-    for (int c0 = 0; c0 < nv; c0 += 32) {
-      const int c = c0 + F.lane;
-      const bool ok = c < nv;
-      const uint32_t k = ok ? ks[c] : 0u;
-      const int dg = ok ? (int)((k >> sh) & 0xffu) : -1 - F.lane;
-      const unsigned peers = __match_any_sync(FULL, dg);
-      if (ok) {
-        const uint32_t at = hist[dg] + (uint32_t)__popc(peers & lt);
-        kd[at] = k;
-        cd[at] = cs[c];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (F.lane >= o) incl += y;
       }
-      __syncwarp();
-      if (ok && (__ffs(peers) - 1) == F.lane) hist[dg] += (uint32_t)__popc(peers);
-      __syncwarp();
+      const int tot = __shfl_sync(FULL, incl, 31);
+      skip |= (tot == nv);
+      offs[dg * 32 + F.lane] = (uint32_t)(base + incl - cnt);
+      base += tot;
     }
+    if (skip) {   // warp-uniform (tot is)
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    for (int i = lo; i < hi; ++i) {
+      const uint32_t k = ks[i];
+      const int dg = (k >> sh) & 0xf;
+      const uint32_t at = offs[dg * 32 + F.lane];
+      offs[dg * 32 + F.lane] = at + 1u;
+      kd[at] = k;
+      cd[at] = cs[i];
+    }
+    __syncwarp();
     uint32_t* tk = ks; ks = kd; kd = tk;
     uint16_t* tc = cs; cs = cd; cd = tc;
   }
@@ -433,7 +437,7 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   // IPM iteration 0, where every weight is exactly 1).
   bool tie = false;
   for (int r = F.lane; r + 1 < nv; r += 32)
-    if (ks[r] == ks[r + 1] && F.d2[order[r]] < F.d2[order[r + 1]]) tie = true;
+    if (ks[r] == ks[r + 1] && d2[order[r]] < d2[order[r + 1]]) tie = true;
   if (__any_sync(FULL, tie)) {
     if (F.lane == 0) {
       int r = 0;
@@ -443,11 +447,11 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
         while (e < nv && ks[e] == key) ++e;
         for (int a = r + 1; a < e; ++a) {   // insertion sort by (d2 desc, column asc)
           const uint16_t ca = order[a];
-          const double wa = F.d2[ca];
+          const double wa = d2[ca];
           int b = a - 1;
           while (b >= r) {
             const uint16_t cb = order[b];
-            const double wb = F.d2[cb];
+            const double wb = d2[cb];
             if (!((wa > wb) || (wa == wb && ca < cb))) break;
             order[b + 1] = cb;
             --b;
@@ -464,22 +468,25 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
 
 // Alg. 7 lines 5-9, the p picks.  DEG1 as a rank bitmap: bit r set <=> the column of rank r
 // currently has exactly one live row; "the maximum-weight column in DEG1" (line 6) is the
-// first set bit.  Pick k: r -> column c = order[r] -> its live row R = xr[c] (XOR of live
-// rows); record it (line 7); kill row R (line 8): the <= d_c + 1 columns of R lose a live row,
-// entering DEG1 at degree 1 and leaving it at degree 0 (line 9).
+// first set bit.  Pick k: r -> its live row R = xrR[r] (XOR of the column's live rows, kept per
+// rank) and column c = order[r]; record it (line 7); kill row R (line 8): the <= d_c + 1 columns
+// of R (their ranks precomputed in rrank[R][.]) lose a live row, entering DEG1 at degree 1 and
+// leaving it at degree 0 (line 9).  The critical path of a pick is three dependent shared-memory
+// loads (xrR, rrank, cntR / xrR) plus the bitmap search and update.
 // Register variant: lane l owns bitmap words l, 32 + l, ... (K per lane), so the search is a
 // ballot and the updates are shuffles — no shared-memory atomics on the pick's critical path.
-template <int K>
-__device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint16_t* order,
-                                               const uint16_t* rank, uint8_t* cnt, uint16_t* xr,
+template <int K, int RS>
+__device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint16_t* __restrict__ order,
+                                               const uint16_t* __restrict__ rrank,
+                                               uint8_t* __restrict__ cntR, uint16_t* __restrict__ xrR,
                                                const unsigned long long* bm, uint16_t* pos,
                                                uint16_t* pcol, uint16_t* prow) {
-  const DCode& C = *F.C;
+  const int W = F.C->W;
   unsigned long long wd[K];
 #pragma unroll
   for (int kk = 0; kk < K; ++kk) {
     const int w = 32 * kk + F.lane;
-    wd[kk] = (w < C.W) ? bm[w] : 0ull;
+    wd[kk] = (w < W) ? bm[w] : 0ull;
   }
   for (int k = 0; k < p; ++k) {
     int r = 0;
@@ -493,30 +500,32 @@ __device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint
         break;
       }
     }
-    const int c = order[r];
-    const int R = xr[c];
+    const int R = xrR[r];
     if (F.lane == 0) {
       pos[R] = (uint16_t)k;
-      pcol[R] = (uint16_t)c;
+      pcol[R] = order[r];
       prow[k] = (uint16_t)R;
     }
-    const int deg = C.chk_deg[R];
-    int upd = -1;   // rank << 1 | set (degree 1) ; -1: no DEG1 change
-    if (F.lane <= deg) {
-      const int cc = (F.lane < deg) ? chk_nb(C, R, F.lane) : (C.n + R);
-      const int nc = (int)cnt[cc] - 1;
-      cnt[cc] = (uint8_t)nc;
-      xr[cc] = (uint16_t)(xr[cc] ^ R);
-      if (nc <= 1) upd = ((int)rank[cc] << 1) | (nc == 1 ? 1 : 0);
+    int upd = -1;   // rank << 1 | (degree now 1) ; -1: no DEG1 change
+    const int rr = (F.lane < RS) ? (int)rrank[R * RS + F.lane] : (int)NONE16;
+    if (rr != (int)NONE16) {
+      const int nc = (int)cntR[rr] - 1;
+      cntR[rr] = (uint8_t)nc;
+      xrR[rr] = (uint16_t)(xrR[rr] ^ R);
+      if (nc <= 1) upd = (rr << 1) | (nc == 1 ? 1 : 0);
     }
-    // apply the (<= d_c + 1) bit updates in the owning lanes
-    for (int t = 0; t <= deg; ++t) {
-      const int u = __shfl_sync(FULL, upd, t);
+    // apply the (<= d_c + 1) bit updates in the owning lanes (shuffles issued back to back)
+    int us[RS];
+#pragma unroll
+    for (int t = 0; t < RS; ++t) us[t] = __shfl_sync(FULL, upd, t);
+#pragma unroll
+    for (int t = 0; t < RS; ++t) {
+      const int u = us[t];
       if (u < 0) continue;
-      const int rr = u >> 1;
-      const int wi = rr >> 6;
+      const int rk = u >> 1;
+      const int wi = rk >> 6;
       if ((wi & 31) == F.lane) {
-        const unsigned long long bit = 1ull << (rr & 63);
+        const unsigned long long bit = 1ull << (rk & 63);
 #pragma unroll
         for (int kk = 0; kk < K; ++kk)
           if ((wi >> 5) == kk) wd[kk] = (u & 1) ? (wd[kk] | bit) : (wd[kk] & ~bit);
@@ -526,16 +535,16 @@ __device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint
   }
 }
 
-// Shared-memory variant for large codes (W > 128 words).
+// Shared-memory bitmap variant for large codes (W > 128 words).
 __device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16_t* order,
-                                             const uint16_t* rank, uint8_t* cnt, uint16_t* xr,
-                                             unsigned long long* bm, uint16_t* pos, uint16_t* pcol,
-                                             uint16_t* prow) {
-  const DCode& C = *F.C;
+                                             const uint16_t* rrank, int RS, uint8_t* cntR,
+                                             uint16_t* xrR, unsigned long long* bm, uint16_t* pos,
+                                             uint16_t* pcol, uint16_t* prow) {
+  const int W = F.C->W;
   for (int k = 0; k < p; ++k) {
     int r = 0;
-    for (int base = 0; base < C.W; base += 32) {
-      unsigned long long wd = (base + F.lane < C.W) ? bm[base + F.lane] : 0ull;
+    for (int base = 0; base < W; base += 32) {
+      unsigned long long wd = (base + F.lane < W) ? bm[base + F.lane] : 0ull;
       unsigned bal = __ballot_sync(FULL, wd != 0ull);
       if (bal) {
         int src = __ffs(bal) - 1;
@@ -544,20 +553,18 @@ __device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16
         break;
       }
     }
-    int c = order[r];
-    int R = xr[c];
+    const int R = xrR[r];
     if (F.lane == 0) {
       pos[R] = (uint16_t)k;
-      pcol[R] = (uint16_t)c;
+      pcol[R] = order[r];
       prow[k] = (uint16_t)R;
     }
-    int deg = C.chk_deg[R];
-    if (F.lane <= deg) {
-      int cc = (F.lane < deg) ? chk_nb(C, R, F.lane) : (C.n + R);
-      int nc = (int)cnt[cc] - 1;
-      cnt[cc] = (uint8_t)nc;
-      xr[cc] = (uint16_t)(xr[cc] ^ R);
-      int rr = rank[cc];
+    __syncwarp();
+    const int rr = (F.lane < RS) ? (int)rrank[R * RS + F.lane] : (int)NONE16;
+    if (rr != (int)NONE16) {
+      const int nc = (int)cntR[rr] - 1;
+      cntR[rr] = (uint8_t)nc;
+      xrR[rr] = (uint16_t)(xrR[rr] ^ R);
       if (nc == 1) atomicOr(&bm[rr >> 6], 1ull << (rr & 63));
       else if (nc == 0) atomicAnd(&bm[rr >> 6], ~(1ull << (rr & 63)));
     }
@@ -565,21 +572,21 @@ __device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16
   }
 }
 
-// Part 2: Alg. 7.  DEG1 (line 4) is a bitmap over ranks; line 6 = first set bit.
-// For each column: number of live rows and XOR of their ids (the unique live row of a
-// degree-1 column).  Pick k records pos[R] = k, pcol[R] = c, prow[k] = R (line 7) and
-// zeroes row R (line 8), updating degrees and DEG1 (line 9).
+// Part 2: Alg. 7 initialisation: rank of every valid column, live-row count and
+// XOR of live rows per rank, the ranks of each present row's columns, the DEG1 bitmap.
 __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
   const DCode& C = *F.C;
   const Layout& L = *F.L;
-  uint16_t* order = F.S<uint16_t>(L.s_order);
+  const uint16_t* order = F.S<uint16_t>(L.s_order);
   uint16_t* rank = F.S<uint16_t>(L.s_rank);
-  uint8_t* cnt = F.S<uint8_t>(L.s_cnt);
-  uint16_t* xr = F.S<uint16_t>(L.s_xr);
+  uint8_t* cntR = F.S<uint8_t>(L.s_cnt);
+  uint16_t* xrR = F.S<uint16_t>(L.s_xr);
   unsigned long long* bm = F.S<unsigned long long>(L.s_bm);
+  uint16_t* rrank = F.S<uint16_t>(L.s_rrank);
   uint16_t* pos = F.S<uint16_t>(L.s_pos);
   uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
   uint16_t* prow = F.S<uint16_t>(L.s_prow);
+  const int RS = L.RS;
   for (int c = F.lane; c < C.Q; c += 32) rank[c] = NONE16;
   for (int w = F.lane; w < C.W; w += 32) bm[w] = 0ull;
   __syncwarp();
@@ -589,6 +596,8 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
   }
   __syncwarp();
   for (int c = F.lane; c < C.Q; c += 32) {
+    const int rk = rank[c];
+    if (rk == (int)NONE16) continue;   // no present row (C-10): never in DEG1
     int cn = 0, x = 0;
     if (c < C.n) {
       uint8_t s = F.sgnV[c];
@@ -598,22 +607,26 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
           ++cn;
           x ^= var_ck(C, c, k);
         }
-    } else if (F.sgnC[c - C.n] & PRESENT) {
+    } else {
       cn = 1;
       x = c - C.n;
     }
-    cnt[c] = (uint8_t)cn;
-    xr[c] = (uint16_t)x;
-    if (cn == 1) {
-      int r = rank[c];
-      atomicOr(&bm[r >> 6], 1ull << (r & 63));
-    }
+    cntR[rk] = (uint8_t)cn;
+    xrR[rk] = (uint16_t)x;
+    if (cn == 1) atomicOr(&bm[rk >> 6], 1ull << (rk & 63));
+  }
+  for (int R = F.lane; R < C.m; R += 32) {
+    if (!(F.sgnC[R] & PRESENT)) continue;
+    const int deg = C.chk_deg[R];
+    for (int t = 0; t < RS; ++t)
+      rrank[R * RS + t] = (t < deg) ? rank[chk_nb(C, R, t)] : (t == deg ? rank[C.n + R] : NONE16);
   }
   __syncwarp();
-  if (C.W <= 32) peel_picks_reg<1>(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
-  else if (C.W <= 64) peel_picks_reg<2>(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
-  else if (C.W <= 128) peel_picks_reg<4>(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
-  else peel_picks_smem(F, p, order, rank, cnt, xr, bm, pos, pcol, prow);
+  if (C.W <= 32 && RS == 8) peel_picks_reg<1, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (C.W <= 32 && RS == 16) peel_picks_reg<1, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (C.W <= 128 && RS == 8) peel_picks_reg<4, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (C.W <= 128 && RS == 16) peel_picks_reg<4, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else peel_picks_smem(F, p, order, rrank, RS, cntR, xrR, bm, pos, pcol, prow);
 }
 
 // Sweep dependencies of the pivot on row R (A_M is upper triangular in pick order):
@@ -786,19 +799,22 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
   nLf = compute_levels<true>(F, p, lvF);
   level_slots(F, p, nLb, lvB, F.offB);
   level_slots(F, p, nLf, lvF, F.offF);
+  // Records (u16, rows < 32768): word 0 = R | diag_neg << 15, then the dependencies
+  // (row | coefficient_neg << 15), unused slots NODEP.  Back: RB words (8 or 16) per pivot,
+  // forward: RF = 4 words per pivot (d_v <= 4) + dinvF = 1 / d^2 of the pivot column.
   for (int k = F.lane; k < p; k += 32) {
-    int R = prow[k];
+    const int R = prow[k];
     int deps[DCMAX];
-    int dn = diag_neg(F, R);
+    const int dn = diag_neg(F, R);
     int nd = back_deps(F, R, deps);
-    int* rb = F.recB + (size_t)lvB[k] * C.RB;
-    rb[0] = R | (nd << 24) | (int)((unsigned)dn << 31);
-    for (int d = 0; d < nd; ++d) rb[1 + d] = deps[d];
+    uint16_t* rb = F.recB + (size_t)lvB[k] * C.RB;
+    rb[0] = (uint16_t)(R | (dn << 15));
+    for (int d = 1; d < C.RB; ++d) rb[d] = (d <= nd) ? (uint16_t)((deps[d - 1] & 0x7fff) | ((deps[d - 1] < 0) << 15)) : NODEP;
     nd = fwd_deps(F, R, deps);
-    int sf = lvF[k];
-    int* rf = F.recF + (size_t)sf * RF;
-    rf[0] = R | (nd << 24) | (int)((unsigned)dn << 31);
-    for (int d = 0; d < nd; ++d) rf[1 + d] = deps[d];
+    const int sf = lvF[k];
+    uint16_t* rf = F.recF + (size_t)sf * RF;
+    rf[0] = (uint16_t)(R | (dn << 15));
+    for (int d = 1; d < RF; ++d) rf[d] = (d <= nd) ? (uint16_t)((deps[d - 1] & 0x7fff) | ((deps[d - 1] < 0) << 15)) : NODEP;
     F.dinvF[sf] = 1.0 / F.d2[pcol[R]];
   }
   __syncwarp();
@@ -847,91 +863,92 @@ struct OffReg {
   }
 };
 
-struct RecB {
-  int4 q[4];   // up to 16 ints: head + <= 15 deps (RB <= 16)
-};
-__device__ __forceinline__ void load_recB(const int* base, int RB, RecB& r) {
-  const int4* p = reinterpret_cast<const int4*>(base);
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (4 * k < RB) r.q[k] = p[k];
-}
-__device__ __forceinline__ int rec_at(const RecB& r, int k) {   // k compile-time after unroll
-  const int* v = reinterpret_cast<const int*>(&r.q[0]);
-  return v[k];
-}
-
 // Back substitution A_M f = r over the level schedule (P:585 stage 1): r in s_r, f in s_f,
-// both indexed by pivot row; f_R is the component of row R's pivot column.
-template <int DCT>
-__device__ __forceinline__ void back_step(const RecB& rec, const double* rS, double* fS) {
-  const int head = rec_at(rec, 0);
-  const int R = head & 0xffffff, nd = (head >> 24) & 0xf;
+// both indexed by pivot row; f_R is the component of row R's pivot column.  A record is RBW
+// uint4 (8 u16 each): [R | neg, dep...].
+template <int RBW>
+__device__ __forceinline__ void back_step(const uint4 (&q)[RBW], const double* rS, double* fS) {
+  const uint16_t* v = reinterpret_cast<const uint16_t*>(&q[0]);
+  const int head = v[0];
+  const int R = head & 0x7fff;
   double acc = rS[R];
 #pragma unroll
-  for (int d = 0; d < DCT - 1; ++d) {
-    if (d < nd) {
-      int dep = rec_at(rec, 1 + d);
-      double fv = fS[dep & 0x7fffffff];
-      acc = (dep < 0) ? acc + fv : acc - fv;
+  for (int d = 1; d < 8 * RBW; ++d) {
+    const int dep = v[d];
+    if (dep != (int)NODEP) {
+      const double fv = fS[dep & 0x7fff];
+      acc = (dep & 0x8000) ? acc + fv : acc - fv;
     }
   }
-  fS[R] = (head < 0) ? -acc : acc;
+  fS[R] = (head & 0x8000) ? -acc : acc;
 }
 
-__device__ ALP_HEAVY void back_sweep(const Frame& F, int nLb) {
-  const DCode& C = *F.C;
+template <int RBW>
+__device__ __forceinline__ void back_sweep_t(const Frame& F, int nLb) {
   const Layout& L = *F.L;
   const double* rS = F.S<double>(L.s_r);
   double* fS = F.S<double>(L.s_f);
-  const int RB = C.RB;
-  if (nLb <= 0) return;
+  const uint4* rec = reinterpret_cast<const uint4*>(F.recB);
   OffReg off;
   off.load(F.offB, nLb, F.lane);
   int a = off(0), b = off(1);
-  RecB cur;
+  uint4 cur[RBW];
   bool hc = a + F.lane < b;
-  if (hc) load_recB(F.recB + (size_t)(a + F.lane) * RB, RB, cur);
+  if (hc) {
+#pragma unroll
+    for (int k = 0; k < RBW; ++k) cur[k] = rec[(size_t)(a + F.lane) * RBW + k];
+  }
   for (int lvl = 0; lvl < nLb; ++lvl) {
     const int c = (lvl + 2 <= nLb) ? off(lvl + 2) : b;
-    RecB nxt;
+    uint4 nxt[RBW];
     const bool hn = (lvl + 1 < nLb) && (b + F.lane < c);
-    if (hn) load_recB(F.recB + (size_t)(b + F.lane) * RB, RB, nxt);
-    if (hc) back_step<DCMAX + 1>(cur, rS, fS);
+    if (hn) {
+#pragma unroll
+      for (int k = 0; k < RBW; ++k) nxt[k] = rec[(size_t)(b + F.lane) * RBW + k];
+    }
+    if (hc) back_step<RBW>(cur, rS, fS);
     for (int s = a + F.lane + 32; s < b; s += 32) {
-      RecB t;
-      load_recB(F.recB + (size_t)s * RB, RB, t);
-      back_step<DCMAX + 1>(t, rS, fS);
+      uint4 t[RBW];
+#pragma unroll
+      for (int k = 0; k < RBW; ++k) t[k] = rec[(size_t)s * RBW + k];
+      back_step<RBW>(t, rS, fS);
     }
     __syncwarp();
     a = b;
     b = c;
-    cur = nxt;
+#pragma unroll
+    for (int k = 0; k < RBW; ++k) cur[k] = nxt[k];
     hc = hn;
   }
 }
 
+__device__ ALP_HEAVY void back_sweep(const Frame& F, int nLb) {
+  if (nLb <= 0) return;
+  if (F.C->RB == 8) back_sweep_t<1>(F, nLb);
+  else back_sweep_t<2>(F, nLb);
+}
 
 // Forward substitution A_M^T z = D_M^-2 f (P:585 stages 2-3); returns this lane's part of
-// z^T r = f^T D_M^-2 f (a sum of squares).
-__device__ __forceinline__ double fwd_step(int4 rec, double dinv, const double* fS, double* zS) {
-  const int head = rec.x;
-  const int R = head & 0xffffff, nd = (head >> 24) & 0xf;
+// z^T r = f^T D_M^-2 f (a sum of squares).  Record: uint2 = 4 u16 [R | neg, dep1..3].
+__device__ __forceinline__ double fwd_step(uint2 rec, double dinv, const double* fS, double* zS) {
+  const int head = rec.x & 0xffff;
+  const int R = head & 0x7fff;
   const double fr = fS[R];
   double acc = fr * dinv;
-  if (nd > 0) {
-    double zv = zS[rec.y & 0x7fffffff];
-    acc = (rec.y < 0) ? acc + zv : acc - zv;
+  const int d1 = rec.x >> 16, d2 = rec.y & 0xffff, d3 = rec.y >> 16;
+  if (d1 != (int)NODEP) {
+    const double zv = zS[d1 & 0x7fff];
+    acc = (d1 & 0x8000) ? acc + zv : acc - zv;
   }
-  if (nd > 1) {
-    double zv = zS[rec.z & 0x7fffffff];
-    acc = (rec.z < 0) ? acc + zv : acc - zv;
+  if (d2 != (int)NODEP) {
+    const double zv = zS[d2 & 0x7fff];
+    acc = (d2 & 0x8000) ? acc + zv : acc - zv;
   }
-  if (nd > 2) {
-    double zv = zS[rec.w & 0x7fffffff];
-    acc = (rec.w < 0) ? acc + zv : acc - zv;
+  if (d3 != (int)NODEP) {
+    const double zv = zS[d3 & 0x7fff];
+    acc = (d3 & 0x8000) ? acc + zv : acc - zv;
   }
-  zS[R] = (head < 0) ? -acc : acc;
+  zS[R] = (head & 0x8000) ? -acc : acc;
   return fr * fr * dinv;
 }
 
@@ -939,13 +956,13 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
   const Layout& L = *F.L;
   const double* fS = F.S<double>(L.s_f);
   double* zS = F.S<double>(L.s_z);
-  const int4* recF = reinterpret_cast<const int4*>(F.recF);   // RF == 4
+  const uint2* recF = reinterpret_cast<const uint2*>(F.recF);   // RF == 4 u16
   double rz = 0.0;
   if (nLf <= 0) return rz;
   OffReg off;
   off.load(F.offF, nLf, F.lane);
   int a = off(0), b = off(1);
-  int4 cur = make_int4(0, 0, 0, 0);
+  uint2 cur = make_uint2(0u, 0u);
   double dcur = 0.0;
   bool hc = a + F.lane < b;
   if (hc) {
@@ -954,7 +971,7 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
   }
   for (int lvl = 0; lvl < nLf; ++lvl) {
     const int c = (lvl + 2 <= nLf) ? off(lvl + 2) : b;
-    int4 nxt = make_int4(0, 0, 0, 0);
+    uint2 nxt = make_uint2(0u, 0u);
     double dnxt = 0.0;
     const bool hn = (lvl + 1 < nLf) && (b + F.lane < c);
     if (hn) {
@@ -1001,6 +1018,7 @@ struct PcgResult {
   int iters, status;
   double relres;       // TRUE ||w - Q dy|| / ||w|| at exit
   double rec_relres;   // recursive ||r|| / ||w|| at exit of the last recursion
+  double relres_prev;  // refine mode: the true relres before the current restart
 };
 
 // l = Q h = A (D^2 (A^T h)) matrix-free over the edges (eq.`Delta y` LHS), h in
@@ -1203,7 +1221,7 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
   }
   __syncwarp();
   const double wn = sqrt(wsum(ww));
-  PcgResult res{0, 0, 0.0, 0.0};
+  PcgResult res{0, 0, 0.0, 0.0, 0.0};
   if (wn == 0.0) return res;
   const double tol = P.pcg_rel_tol * wn;                       // acceptance (C-9)
   double itol = fmin(itol_rel, P.pcg_rel_tol) * wn;            // recursion target
@@ -1222,7 +1240,8 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
     int st = ST_PCG_MAXITER, past = -1, since_min = 0;
     double rrmin = 1e308, rr = 0.0;
     long long tk = clock64();
-    while (it < cap) {
+    const int cap_run = (restart > 0) ? min(cap, it + 200) : cap;   // a refinement restart gets <= 200
+    while (it < cap_run) {
       ALP_TICK(F, CY_PCG, tk);
       const double hl = spmv<false>(F);   // line 6: l = Q h
       ALP_TICK(F, CY_SPMV, tk);
@@ -1326,10 +1345,19 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
       dn = sqrt(wsum(dn));
       yn = sqrt(wsum(yn));
     }
+    if (restart > 0 && st != 0) {
+      // a refinement restart that did not converge: keep dy from before it (the last good one)
+      for (int j = F.lane; j < C.m; j += 32) F.dy[j] = F.v[j];
+      __syncwarp();
+      res.status = (res.relres_prev > P.pcg_rel_tol) ? ST_PCG_FLOOR : 0;
+      res.relres = res.relres_prev;
+      break;
+    }
     if (st != 0 || restart == PCG_REFINE_MAX || (restart > 0 && (dn <= 1e-13 * yn || dn > 0.5 * prev_trn))) {
       if (st == 0 && trn > tol) res.status = ST_PCG_FLOOR;
       break;
     }
+    res.relres_prev = res.relres;
     if (restart > 0) prev_trn = dn;
     for (int j = F.lane; j < C.m; j += 32) F.v[j] = F.dy[j];   // dy before the next correction
     __syncwarp();

@@ -53,12 +53,7 @@ def _exact_job(job):
         A, rows = dense_step_matrix(code, sy.masks[s])
         w2 = step_weights(code, sy.d[s], rows)
         col, row = mts_columnwise(A, w2)
-        y8 = step_solve_exact(A, w2, sy.r[s][rows], refine=8)
-        y4 = step_solve_exact(A, w2, sy.r[s][rows], refine=4)
-        # the extended-precision solve is itself limited (longdouble, kappa up to ~1e18): its
-        # uncertainty is estimated from how far 4 and 8 refinement steps apart still move
-        unc = float(np.linalg.norm(y4 - y8) / max(np.linalg.norm(y8), 1e-300))
-        out.append((y8, col, row, unc))
+        out.append((step_solve_exact(A, w2, sy.r[s][rows]), col, row))
     return out
 
 
@@ -77,9 +72,9 @@ def oracle_decode(cfg: int, frames, snr_idx: int = 0, variant: str = "A", llr_sc
         return [o for part in ex.map(_decode_job, jobs) for o in part]
 
 
-def oracle_step_exact(systems, lo: float = -6, hi: float = 6, chunk: int = 4) -> list:
+def oracle_step_exact(systems, lo: float = -6, hi: float = 6, chunk: int = 2) -> list:
     """step_solve_exact (extended-precision Cholesky + refinement) and the Alg. 7 heap pivot
-    sequence on config-5 systems: list of (dy, pivot cols, pivot rows, reference uncertainty)."""
+    sequence on config-5 systems: list of (dy, pivot cols, pivot rows)."""
     systems = list(systems)
     jobs = [(systems[i:i + chunk], lo, hi) for i in range(0, len(systems), chunk)]
     with _pool(len(jobs)) as ex:

@@ -279,13 +279,22 @@ def test_config1_plain_cg_decode():
     assert_certified(code, fb.llr, g)
 
 
-def test_large_code_fails_loudly():
-    """Config 4 (n = 32,000) without the large-n path: the library must refuse with
-    ALP_ERR_UNSUPPORTED, never fall back."""
-    alp = _alp()
-    from synth.codes import regular_code
-    code = regular_code(32000, 3, 6, seed=1004)
-    c = alp.Code.from_synth(code)
-    with pytest.raises(alp.AlpError) as ei:
-        alp.decode(c, torch.zeros((2, code.n), dtype=torch.float64, device="cuda"))
-    assert ei.value.status == -3
+def test_config4_golden_frames():
+    """Config 4 (n = 32,000, m = 16,000, 2.2 dB; the large-n layout: phase window in global
+    memory): the first frames against the oracle outputs written offline by
+    tools/make_c4_golden.py (calls only oracle/), P1-P3 + P6 and the LP count."""
+    import glob
+    files = sorted(glob.glob(os.path.join(GOLD, "c4_oracle_f*.npz")))
+    assert files, "tests/golden/c4_oracle_f*.npz missing (python tools/make_c4_golden.py 0 1)"
+    gold = [dict(np.load(f)) for f in files]
+    frames = [int(g["frame"]) for g in gold]
+    code = config_code(4)
+    fb = config_frames(4, frames=frames, code=code)
+    for k, g in enumerate(gold):
+        assert abs(float(g["llr_checksum"]) - float(np.sum(fb.llr[k] ** 2))) <= 1e-9 * float(g["llr_checksum"])
+    g = gpu_decode(code, fb.llr)
+    orc = [dict(u=o["u"], hard=o["hard"], obj=float(o["obj"]), g_max=float(o["g_max"]), cert=int(o["cert"]),
+                status=int(o["status"]), lp_solves=int(o["lp_solves"]), ipm_iters=int(o["ipm_iters"]),
+                chol_fixes=int(o["chol_fixes"])) for o in gold]
+    parity("C4_golden", code, fb.llr, g, orc)
+    assert_certified(code, fb.llr, g)

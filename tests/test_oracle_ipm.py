@@ -137,12 +137,12 @@ def _exact_rational_solve(A, d2, w):
     return np.array([float(M[k][p] / M[k][k]) for k in range(p)])
 
 
-@pytest.mark.parametrize("seed,span", [(0, 2), (1, 8), (2, 14)])
+@pytest.mark.parametrize("seed,span", [(0, 2), (1, 8), (2, 14), (3, 20), (4, 24)])
 def test_step_solve_exact_matches_rational_solution(seed, span):
     """Pin: on small config-5-like systems (one random odd cut per check, slack columns, d^2
-    log-uniform over span decades, kappa up to ~1e15) the extended-precision solve equals
-    the exact rational solution to 1e-10 relative (observed <= 6e-12 at kappa 1e10, where
-    fp64 Cholesky is off by ~4e-9)."""
+    log-uniform over span decades, kappa up to ~1e20+) the refined solve equals the exact
+    rational solution (Gaussian elimination in fractions) to 1e-14 relative; fp64 Cholesky is
+    off by ~4e-9 already at kappa 1e10, long-double refinement alone by up to ~1e-7."""
     from synth import c5_systems
     from tests.helpers import dense_step_matrix, step_weights
     code = regular_code(24, 3, 6, seed=10 + seed)
@@ -152,7 +152,7 @@ def test_step_solve_exact_matches_rational_solution(seed, span):
     w = sy.r[0][rows]
     exact = _exact_rational_solve(A, d2, w)
     got = step_solve_exact(A, d2, w)
-    assert np.linalg.norm(got - exact) <= 1e-10 * np.linalg.norm(exact)
+    assert np.linalg.norm(got - exact) <= 1e-14 * np.linalg.norm(exact)
 
 
 def test_step_solve_exact_agrees_with_lapack_when_well_conditioned():
