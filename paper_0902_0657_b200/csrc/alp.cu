@@ -43,7 +43,7 @@ struct IpmOut {
 // =====================================================================================
 __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
                             double bmax, double cmax, long long frame_id, int lp_id) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
   const double q = (double)(n + p);
   // restrict-qualified views: the arrays never alias, which lets the unrolled loops below
@@ -300,7 +300,7 @@ struct DecodeOut {
 // MALP-A / MALP-B decode of one frame (Alg. 3; outputs P:143, C-11..C-15).
 __device__ void decode_frame(Frame& F, const Params& P, const double* g, long long f,
                              const DecodeOut& O) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const int n = C.n, m = C.m, lane = F.lane;
   double cm = 0.0;
   for (int i = lane; i < n; i += 32) {

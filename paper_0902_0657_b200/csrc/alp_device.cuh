@@ -224,7 +224,7 @@ __device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
 // =====================================================================================
 __device__ ALP_HEAVY void build_signs(const Frame& F, bool want_b, int& p_out, int& nact_out,
                             double& bmax_out) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   int p = 0;
   double bmax = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
@@ -284,7 +284,7 @@ __device__ ALP_HEAVY void build_signs(const Frame& F, bool want_b, int& p_out, i
 // Returns warp-uniform "changed".
 // =====================================================================================
 __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   bool changed = false;
   for (int j = F.lane; j < C.m; j += 32) {
     int deg = C.chk_deg[j];
@@ -343,7 +343,7 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
 // u16[Q] must not overlap them (layout: s_order, then s_sortk).
 // =====================================================================================
 __device__ ALP_HEAVY int sort_columns(const Frame& F) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   const uint16_t* __restrict__ sgnC = F.sgnC;
   const uint8_t* __restrict__ sgnV = F.sgnV;
@@ -377,7 +377,7 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   // [l*ch, (l+1)*ch) of the current sequence, so lane order = sequence order and the scatter
   // (digit base + earlier lanes' counts + this lane's running count) is stable.  Per-lane digit
   // counts live in registers (four packed u64, 16 bits per digit: ch <= 65535).
-  const int ch = (nv + 31) >> 5;
+  const int ch = ((nv + 31) >> 5) | 1;   // odd chunk stride: the lanes' u32 loads hit distinct banks
   const int lo = min(nv, F.lane * ch), hi = min(nv, lo + ch);
   uint32_t* ks = kA;
   uint32_t* kd = kB;
@@ -514,23 +514,29 @@ __device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint
       xrR[rr] = (uint16_t)(xrR[rr] ^ R);
       if (nc <= 1) upd = (rr << 1) | (nc == 1 ? 1 : 0);
     }
-    // apply the (<= d_c + 1) bit updates in the owning lanes (shuffles issued back to back)
+    // apply the (<= d_c + 1) bit updates in the owning lanes: shuffles issued back to back,
+    // branch-free set / clear masks per owned word (a column changes at most once per pick)
     int us[RS];
 #pragma unroll
     for (int t = 0; t < RS; ++t) us[t] = __shfl_sync(FULL, upd, t);
+    unsigned long long setm[K], clrm[K];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) setm[kk] = clrm[kk] = 0ull;
 #pragma unroll
     for (int t = 0; t < RS; ++t) {
       const int u = us[t];
-      if (u < 0) continue;
       const int rk = u >> 1;
-      const int wi = rk >> 6;
-      if ((wi & 31) == F.lane) {
-        const unsigned long long bit = 1ull << (rk & 63);
+      const bool mine = (u >= 0) && (((rk >> 6) & 31) == F.lane);
+      const unsigned long long bit = mine ? (1ull << (rk & 63)) : 0ull;
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk)
-          if ((wi >> 5) == kk) wd[kk] = (u & 1) ? (wd[kk] | bit) : (wd[kk] & ~bit);
+      for (int kk = 0; kk < K; ++kk) {
+        const unsigned long long b = ((rk >> 11) == kk) ? bit : 0ull;
+        setm[kk] |= (u & 1) ? b : 0ull;
+        clrm[kk] |= (u & 1) ? 0ull : b;
       }
     }
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) wd[kk] = (wd[kk] | setm[kk]) & ~clrm[kk];
     __syncwarp();
   }
 }
@@ -575,7 +581,7 @@ __device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16
 // Part 2: Alg. 7 initialisation: rank of every valid column, live-row count and
 // XOR of live rows per rank, the ranks of each present row's columns, the DEG1 bitmap.
 __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   const uint16_t* order = F.S<uint16_t>(L.s_order);
   uint16_t* rank = F.S<uint16_t>(L.s_rank);
@@ -634,7 +640,7 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
 //  fwd   (A_M^T z = g): the other present rows of column C_k (killed earlier)
 // Encoded row | (coefficient < 0) << 31.
 __device__ __forceinline__ int back_deps(const Frame& F, int R, int* deps) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const uint16_t* poc = F.S<uint16_t>(F.L->s_poc);
   int deg = C.chk_deg[R];
   uint16_t s = F.sgnC[R];
@@ -649,7 +655,7 @@ __device__ __forceinline__ int back_deps(const Frame& F, int R, int* deps) {
   return nd;
 }
 __device__ __forceinline__ int fwd_deps(const Frame& F, int R, int* deps) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   int c = F.S<uint16_t>(F.L->s_pcol)[R];
   int nd = 0;
   if (c < C.n) {
@@ -666,7 +672,7 @@ __device__ __forceinline__ int fwd_deps(const Frame& F, int R, int* deps) {
 }
 // sign of the diagonal entry A[R, C_k]
 __device__ __forceinline__ int diag_neg(const Frame& F, int R) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   int c = F.S<uint16_t>(F.L->s_pcol)[R];
   if (c >= C.n) return 0;
   uint8_t s = F.sgnV[c];
@@ -770,7 +776,7 @@ __device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* of
 //  back  recB[slot*RB]: head = R | nd << 24 | diag_neg << 31, then nd deps (row | neg << 31)
 //  fwd   recF[slot*RF]: same head/deps; dinvF[slot] = 1 / d^2 of the pivot column
 __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   long long t0 = clock64();
   sort_columns(F);
@@ -822,7 +828,7 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
 
 // Pivot sequence output (ipm_step_pcg debug/parity): rows[k], cols[k], -1 past p.
 __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const uint16_t* prow = F.S<uint16_t>(F.L->s_prow);
   const uint16_t* pcol = F.S<uint16_t>(F.L->s_pcol);
   for (int k = F.lane; k < C.m; k += 32) {
@@ -956,7 +962,8 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
   const Layout& L = *F.L;
   const double* fS = F.S<double>(L.s_f);
   double* zS = F.S<double>(L.s_z);
-  const uint2* recF = reinterpret_cast<const uint2*>(F.recF);   // RF == 4 u16
+  const uint2* __restrict__ recF = reinterpret_cast<const uint2*>(F.recF);   // RF == 4 u16
+  const double* __restrict__ dinvF = F.dinvF;
   double rz = 0.0;
   if (nLf <= 0) return rz;
   OffReg off;
@@ -967,7 +974,7 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
   bool hc = a + F.lane < b;
   if (hc) {
     cur = recF[a + F.lane];
-    dcur = F.dinvF[a + F.lane];
+    dcur = dinvF[a + F.lane];
   }
   for (int lvl = 0; lvl < nLf; ++lvl) {
     const int c = (lvl + 2 <= nLf) ? off(lvl + 2) : b;
@@ -976,10 +983,10 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
     const bool hn = (lvl + 1 < nLf) && (b + F.lane < c);
     if (hn) {
       nxt = recF[b + F.lane];
-      dnxt = F.dinvF[b + F.lane];
+      dnxt = dinvF[b + F.lane];
     }
     if (hc) rz += fwd_step(cur, dcur, fS, zS);
-    for (int s = a + F.lane + 32; s < b; s += 32) rz += fwd_step(recF[s], F.dinvF[s], fS, zS);
+    for (int s = a + F.lane + 32; s < b; s += 32) rz += fwd_step(recF[s], dinvF[s], fS, zS);
     __syncwarp();
     a = b;
     b = c;
@@ -995,7 +1002,7 @@ constexpr int PC_MTS = 0, PC_NONE = 1;
 
 __device__ __forceinline__ void precond_apply(const Frame& F, int mode, int nLb, int nLf,
                                               double& rz) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   double* rS = F.S<double>(L.s_r);
   double* zS = F.S<double>(L.s_z);
@@ -1028,23 +1035,29 @@ struct PcgResult {
 // check pass of spmv: l_j = sum_i A_ji t_i + d2_{n+j} h_j, two checks per lane per step,
 // DCT >= the code's maximum check degree (compile-time, so the gathers unroll exactly)
 template <bool ABS, int DCT>
-__device__ __forceinline__ double spmv_checks(const Frame& F, const double* hS, const double* tS) {
-  const DCode& C = *F.C;
+__device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, const double* __restrict__ hS,
+                                              const double* __restrict__ tS) {
+  const uint16_t* __restrict__ sgnC = F.sgnC;
+  const uint16_t* __restrict__ chk_var = C.chk_var;
+  const uint8_t* __restrict__ chk_deg = C.chk_deg;
+  const double* __restrict__ d2s_ = F.d2 + C.n;
+  double* __restrict__ lout = F.l;
+  const int m = C.m, dc = C.dc;
   double hl = 0.0;
-  for (int j0 = F.lane; j0 < C.m; j0 += 64) {
+  for (int j0 = F.lane; j0 < m; j0 += 64) {
     uint16_t sc[2];
     double hj[2], d2s[2];
     int in[2][DCT];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int j = j0 + 32 * u;
-      const bool ok = j < C.m;
-      sc[u] = ok ? F.sgnC[j] : (uint16_t)0;
-      const int deg = ok ? (int)C.chk_deg[j] : 0;
+      const bool ok = j < m;
+      sc[u] = ok ? sgnC[j] : (uint16_t)0;
+      const int deg = ok ? (int)chk_deg[j] : 0;
       hj[u] = ok ? hS[j] : 0.0;
-      d2s[u] = ok ? F.d2[C.n + j] : 0.0;
+      d2s[u] = ok ? d2s_[j] : 0.0;
 #pragma unroll
-      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? chk_nb(C, j, t) : -1;
+      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)chk_var[j * dc + t] : -1;
     }
     double acc[2];
 #pragma unroll
@@ -1064,7 +1077,7 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const double* hS, 
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int j = j0 + 32 * u;
-      if (j < C.m && (sc[u] & PRESENT)) F.l[j] = acc[u];
+      if (j < m && (sc[u] & PRESENT)) lout[j] = acc[u];
     }
   }
   return hl;
@@ -1072,29 +1085,33 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const double* hS, 
 
 template <bool ABS>
 __device__ ALP_HEAVY double spmv(const Frame& F) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
-  const double* hS = F.S<double>(L.s_h);
-  double* tS = F.S<double>(L.s_t);
+  const double* __restrict__ hS = F.S<double>(L.s_h);
+  double* __restrict__ tS = F.S<double>(L.s_t);
+  const uint8_t* __restrict__ sgnV = F.sgnV;
+  const uint16_t* __restrict__ var_chk = C.var_chk;
+  const double* __restrict__ d2 = F.d2;
+  const int n = C.n, dvm = C.dv;
   const int dcs = C.dc;
   double hl = 0.0;
   // variable pass, U variables per lane per step: all their index / sign / weight loads are
   // issued before any gather, and all gathers before any store (the shared-memory store of
   // t would otherwise block hoisting the next variable's loads)
   constexpr int U = 2;
-  for (int i0 = F.lane; i0 < C.n; i0 += 32 * U) {
+  for (int i0 = F.lane; i0 < n; i0 += 32 * U) {
     uint8_t sv[U];
     double dv[U];
     int jn[U][DVMAX];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + 32 * u;
-      const bool ok = i < C.n;
-      sv[u] = ok ? F.sgnV[i] : (uint8_t)0;
-      dv[u] = ok ? F.d2[i] : 0.0;
+      const bool ok = i < n;
+      sv[u] = ok ? sgnV[i] : (uint8_t)0;
+      dv[u] = ok ? d2[i] : 0.0;
 #pragma unroll
       for (int k = 0; k < DVMAX; ++k)
-        jn[u][k] = (ok && k < C.dv && ((sv[u] >> k) & 1)) ? var_ck(C, i, k) : -1;
+        jn[u][k] = (ok && k < dvm && ((sv[u] >> k) & 1)) ? (int)var_chk[i * dvm + k] : -1;
     }
     double acc[U];
 #pragma unroll
@@ -1112,7 +1129,7 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + 32 * u;
-      if (i < C.n && (sv[u] & 0xf)) {
+      if (i < n && (sv[u] & 0xf)) {
         const double tv = dv[u] * acc[u];
         tS[i] = tv;
         hl += acc[u] * tv;
@@ -1121,9 +1138,9 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
   }
   __syncwarp();
   // check pass, specialised on the maximum check degree so the unrolled gathers match it
-  if (dcs <= 6) hl += spmv_checks<ABS, 6>(F, hS, tS);
-  else if (dcs <= 12) hl += spmv_checks<ABS, 12>(F, hS, tS);
-  else hl += spmv_checks<ABS, DCMAX>(F, hS, tS);
+  if (dcs <= 6) hl += spmv_checks<ABS, 6>(F, C, hS, tS);
+  else if (dcs <= 12) hl += spmv_checks<ABS, 12>(F, C, hS, tS);
+  else hl += spmv_checks<ABS, DCMAX>(F, C, hS, tS);
   __syncwarp();
   return ABS ? 0.0 : wsum(hl);
 }
@@ -1156,7 +1173,7 @@ __device__ __forceinline__ DD dd_mul(DD a, double b) {
 // (A^T dy)_i recomputed per edge); rounded r to rS, returns ||r||^2.  The residual itself is then
 // accurate far below the fp64 evaluation floor, which is what lets refinement converge.
 __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   double acc = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
     const uint16_t sc = F.sgnC[j];
@@ -1203,7 +1220,7 @@ __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
 // ST_PCG_BREAKDOWN, ST_PCG_FLOOR (refine mode).  w is read from F.w; dy accumulates in F.dy.
 __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mode, int nLb, int nLf,
                                          double itol_rel, bool refine) {
-  const DCode& C = *F.C;
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   double* hS = F.S<double>(L.s_h);
   double* rS = F.S<double>(L.s_r);
@@ -1296,10 +1313,13 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
       }
       const double nu = rz_new / rz;   // line 11
       rz = rz_new;
+      {
+        const uint16_t* __restrict__ sc = F.sgnC;
 #pragma unroll 4
-      for (int j = F.lane; j < C.m; j += 32) {
-        if (!(F.sgnC[j] & PRESENT)) continue;
-        hS[j] = zS[j] + nu * hS[j];   // line 12
+        for (int j = F.lane; j < C.m; j += 32) {
+          if (!(sc[j] & PRESENT)) continue;
+          hS[j] = zS[j] + nu * hS[j];   // line 12
+        }
       }
       __syncwarp();
     }
