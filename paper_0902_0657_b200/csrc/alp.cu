@@ -12,7 +12,7 @@
 #include <vector>
 
 #include "alp.h"
-#include "alp_device.cuh"
+#include "alp_device.cuh"   // mode-independent types (first inclusion also defines them)
 
 namespace alp {
 
@@ -25,267 +25,6 @@ __device__ TraceRec* g_trace = nullptr;
 __device__ int g_trace_cap = 0;
 __device__ int g_trace_n = 0;
 
-struct IpmOut {
-  int iters, status, pcg_iters, solves, p4_fail, true_fail;
-  double pcg_bytes, max_rec, max_true;
-};
-
-// =====================================================================================
-// Infeasible primal-dual path-following IPM (§IV-B) on the current pool LP
-// min c^T x, A x = b, x >= 0 (q = n + p columns; absent slack columns excluded).
-// Start x = z = s0 e, y = 0, s0 = max(1, ||b||, ||c||) (C-7).  Per iteration:
-// r_b = b - A x, r_c = c - A^T y - z, gap = x^T z; stop per C-8; mu = sigma gap / q
-// (eq.`update mu`, C-5); D^2 = X Z^-1, r_e = mu e - XZe; w = r_b + A (D^2 r_c - Z^-1 r_e)
-// (eq.`Delta y`); PCG for dy; dx = D^2 A^T dy - D^2 r_c + Z^-1 r_e (eq.`Delta x`);
-// dz = X^-1 (r_e - Z dx) (eq.`Delta z`); ratio test with eta (C-6); update.
-// Arrays: v holds r_c then D^2 r_c - Z^-1 r_e then dx; d2 holds D^2 then dz; w holds r_b
-// then the PCG right-hand side.
-// =====================================================================================
-__device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
-                            double bmax, double cmax, long long frame_id, int lp_id) {
-  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
-  const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
-  const double q = (double)(n + p);
-  // restrict-qualified views: the arrays never alias, which lets the unrolled loops below
-  // issue the next lane-iterations' loads before this one's stores
-  double* __restrict__ X = F.x;
-  double* __restrict__ Z = F.z;
-  double* __restrict__ Y = F.y;
-  double* __restrict__ V = F.v;
-  const double* __restrict__ B = F.b;
-  // (d2, w and dy are shared with build_precond / pcg_solve: plain pointers)
-  double* D2 = F.d2;
-  double* W = F.w;
-  const double* DY = F.dy;
-  const uint16_t* __restrict__ SC = F.sgnC;
-  const uint8_t* __restrict__ SV = F.sgnV;
-  double* __restrict__ RBv = F.rb;   // r_b and r_c of the current iterate (kept for the recovery)
-  double* __restrict__ RCv = F.rc;
-  const double s0 = fmax(1.0, fmax(bmax, cmax));
-  for (int c = lane; c < Q; c += 32) {
-    bool valid = (c < n) || (SC[c - n] & PRESENT);
-    X[c] = valid ? s0 : 0.0;
-    Z[c] = valid ? s0 : 0.0;
-  }
-  for (int j = lane; j < m; j += 32) Y[j] = 0.0;
-  __syncwarp();
-  IpmOut out{0, 0, 0, 0, 0, 0, 0.0, 0.0, 0.0};
-  long long tk = clock64();
-  // algorithmic bytes per PCG iteration of this LP
-  const double Bmin = 8.0 * (nact + p) + 48.0 * p + 5.0 * p + 2.0 * m;
-  int it = 0;
-  while (true) {
-    double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
-#pragma unroll 4
-    for (int j = lane; j < m; j += 32) {
-      uint16_t s = SC[j];
-      if (!(s & PRESENT)) continue;
-      int deg = C.chk_deg[j];
-      double acc = B[j] - X[n + j];
-      for (int t = 0; t < deg; ++t) {
-        double xi = X[chk_nb(C, j, t)];
-        acc = ((s >> t) & 1) ? acc + xi : acc - xi;
-      }
-      W[j] = acc;
-      RBv[j] = acc;
-      rbn = fmax(rbn, fabs(acc));
-      double rc = -Y[j] - Z[n + j];
-      V[n + j] = rc;
-      RCv[n + j] = rc;
-      rcn = fmax(rcn, fabs(rc));
-      gap += X[n + j] * Z[n + j];
-    }
-#pragma unroll 4
-    for (int i = lane; i < n; i += 32) {
-      double ci = fabs(g[i]);
-      uint8_t s = SV[i];
-      int dv = C.var_deg[i];
-      double acc = ci - Z[i];
-      for (int k = 0; k < dv; ++k) {
-        if (!((s >> k) & 1)) continue;
-        double yj = Y[var_ck(C, i, k)];
-        acc = ((s >> (4 + k)) & 1) ? acc + yj : acc - yj;
-      }
-      V[i] = acc;
-      RCv[i] = acc;
-      rcn = fmax(rcn, fabs(acc));
-      double xi = X[i];
-      gap += xi * Z[i];
-      cx += ci * xi;
-    }
-    __syncwarp();
-    rbn = wmax(rbn);
-    rcn = wmax(rcn);
-    gap = wsum(gap);
-    cx = wsum(cx);
-    if (gap <= P.gap_tol * (1.0 + fabs(cx)) && rbn <= P.feas_tol * (1.0 + bmax) &&
-        rcn <= P.feas_tol * (1.0 + cmax))
-      break;
-    if (it >= P.ipm_max_iter) {
-      out.status |= ST_IPM_MAXITER;
-      break;
-    }
-    const double mu = P.sigma * gap / q;
-#pragma unroll 4
-    for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(SC[c - n] & PRESENT)) continue;
-      double xc = X[c], zc = Z[c];
-      const double iz = 1.0 / zc;   // one division for D^2 = X Z^-1 and Z^-1 r_e
-      double d2 = xc * iz;
-      double re = mu - xc * zc;
-      D2[c] = d2;
-      V[c] = d2 * V[c] - re * iz;
-    }
-    __syncwarp();
-#pragma unroll 4
-    for (int j = lane; j < m; j += 32) {
-      uint16_t s = SC[j];
-      if (!(s & PRESENT)) continue;
-      int deg = C.chk_deg[j];
-      double acc = W[j] + V[n + j];
-      for (int t = 0; t < deg; ++t) {
-        double vi = V[chk_nb(C, j, t)];
-        acc = ((s >> t) & 1) ? acc - vi : acc + vi;
-      }
-      W[j] = acc;
-    }
-    __syncwarp();
-    int nLb = 0, nLf = 0;
-    const bool mtm = (P.precond == 0);
-    ALP_TICK(F, CY_IPM, tk);
-    // the Alg. 7 triangular set is both the PCG preconditioner (precond = 0) and the basis of
-    // the step's feasibility correction (C-32), so plain CG builds it too when that is on
-    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf);
-    ALP_TICK(F, CY_BUILD, tk);
-    // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to well
-    // below z ~ mu on the basic columns, so late in the IPM the recursion aims at
-    // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); P4 acceptance is pcg_rel_tol.  An inexact
-    // dy is admissible because the recovery below keeps every KKT row but the complementarity
-    // of the basis columns exact (C-32).
-    const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, P.pcg_forcing * mu));
-    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, inner, false);
-    tk = clock64();
-    out.status |= pr.status;
-    out.solves += 1;
-    out.p4_fail += (pr.status != 0) ? 1 : 0;
-    out.true_fail += (pr.relres > P.pcg_rel_tol) ? 1 : 0;
-    out.max_rec = fmax(out.max_rec, pr.rec_relres);
-    out.max_true = fmax(out.max_true, pr.relres);
-    double dmn = 1e308, dmx = 0.0;
-    if (g_trace) {
-      for (int c = lane; c < Q; c += 32) {
-        if (c >= n && !(SC[c - n] & PRESENT)) continue;
-        dmn = fmin(dmn, D2[c]);
-        dmx = fmax(dmx, D2[c]);
-      }
-      dmn = wmin(dmn);
-      dmx = wmax(dmx);
-    }
-    out.pcg_iters += pr.iters;
-    out.pcg_bytes += (double)pr.iters * Bmin;
-    // Newton recovery (eq.`Delta x`, eq.`Delta z` P:480-481).  dz is taken in the algebraically
-    // identical form dz = r_c - A^T dy (eliminate dx from eq.`Delta z`), which keeps the dual
-    // equation A^T(y+dy) + z + dz = c exact for ANY dy; with dx from eq.`Delta x` the
-    // complementarity row Z dx + X dz = r_e is then exact too, so an inexact PCG dy only leaves
-    // the primal row off by the step residual rho = r_b - A dx = w - Q dy.  That residual is
-    // moved onto the preconditioner's basis columns: A_M f = rho (the back sweep of P:585),
-    // dx_M += f, so A dx = r_b holds to rounding (reading C-32; R-1).
-#pragma unroll 4
-    for (int i = lane; i < n; i += 32) {
-      uint8_t s = SV[i];
-      int dv = C.var_deg[i];
-      double atdy = 0.0;
-      for (int k = 0; k < dv; ++k) {
-        if (!((s >> k) & 1)) continue;
-        double d = DY[var_ck(C, i, k)];
-        atdy = ((s >> (4 + k)) & 1) ? atdy - d : atdy + d;
-      }
-      const double dx = D2[i] * atdy - V[i];
-      V[i] = dx;
-      D2[i] = RCv[i] - atdy;   // dz
-    }
-    for (int j = lane; j < m; j += 32) {
-      if (!(SC[j] & PRESENT)) continue;
-      const int c = n + j;
-      const double dx = D2[c] * DY[j] - V[c];
-      V[c] = dx;
-      D2[c] = RCv[c] - DY[j];
-    }
-    __syncwarp();
-    if (P.basis_correction && nLb > 0) {
-      double* rS = F.S<double>(F.L->s_r);
-      const double* fS = F.S<double>(F.L->s_f);
-      for (int j = lane; j < m; j += 32) {
-        uint16_t s = SC[j];
-        double rho = 0.0;
-        if (s & PRESENT) {
-          int deg = C.chk_deg[j];
-          double acc = RBv[j] - V[n + j];
-          for (int t = 0; t < deg; ++t) {
-            double xi = V[chk_nb(C, j, t)];
-            acc = ((s >> t) & 1) ? acc + xi : acc - xi;
-          }
-          rho = acc;
-        }
-        rS[j] = rho;
-      }
-      __syncwarp();
-      back_sweep(F, nLb);   // f = A_M^-1 rho, f_R = component of row R's pivot column
-      __syncwarp();
-      for (int j = lane; j < m; j += 32) {
-        const uint16_t c = F.pcolR[j];
-        if (c != NONE16) V[c] += fS[j];
-      }
-      __syncwarp();
-    }
-    // ratio test (C-6)
-    double ax = 1e308, az = 1e308;
-#pragma unroll 4
-    for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(SC[c - n] & PRESENT)) continue;
-      const double dx = V[c], dz = D2[c];
-      if (dx < 0.0) ax = fmin(ax, -X[c] / dx);
-      if (dz < 0.0) az = fmin(az, -Z[c] / dz);
-    }
-    ax = wmin(ax);
-    az = wmin(az);
-    const double bP = fmin(1.0, P.eta * ax);
-    const double bD = fmin(1.0, P.eta * az);
-    if (g_trace) {
-      if (lane == 0) {
-        int slot = atomicAdd(&g_trace_n, 1);
-        if (slot < g_trace_cap)
-          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, pr.relres, pr.rec_relres, dmn, dmx, mu, rbn, rcn, gap, bP, bD};
-      }
-    }
-    bool bad = false;
-#pragma unroll 4
-    for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(SC[c - n] & PRESENT)) continue;
-      double xn = X[c] + bP * V[c];
-      double zn = Z[c] + bD * D2[c];
-      X[c] = xn;
-      Z[c] = zn;
-      bad |= !isfinite(xn) || !isfinite(zn);
-    }
-    for (int j = lane; j < m; j += 32) {
-      if (!(SC[j] & PRESENT)) continue;
-      double yn = Y[j] + bD * DY[j];
-      Y[j] = yn;
-      bad |= !isfinite(yn);
-    }
-    __syncwarp();
-    ++it;
-    if (__any_sync(FULL, bad)) {
-      out.status |= ST_NUMERIC;
-      break;
-    }
-  }
-  ALP_TICK(F, CY_IPM, tk);
-  out.iters = it;
-  return out;
-}
-
 struct DecodeOut {
   uint8_t* hard;
   double* objective;
@@ -296,181 +35,6 @@ struct DecodeOut {
   double* y_out;
   uint16_t* mask_out;
 };
-
-// MALP-A / MALP-B decode of one frame (Alg. 3; outputs P:143, C-11..C-15).
-__device__ void decode_frame(Frame& F, const Params& P, const double* g, long long f,
-                             const DecodeOut& O) {
-  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
-  const int n = C.n, m = C.m, lane = F.lane;
-  double cm = 0.0;
-  for (int i = lane; i < n; i += 32) {
-    double gi = g[i];
-    uint8_t fl = gi < 0.0;  // eq.`initial constraints` P:147-155: u^0 = hard decision
-    F.flip[i] = fl;
-    F.u[i] = fl ? 1.0 : 0.0;
-    cm = fmax(cm, fabs(gi));
-  }
-  for (int j = lane; j < m; j += 32) {
-    F.mask[j] = 0;
-    F.y[j] = 0.0;
-  }
-  const double cmax = wmax(cm);
-  __syncwarp();
-  int status = 0, lp_solves = 0, ipm_iters = 0, pcg_iters = 0, max_p = 0;
-  int solves = 0, p4_fail = 0, true_fail = 0;
-  double max_rec = 0.0, max_true = 0.0;
-  bool last_lp_bad = false;   // the last solved LP did not converge (IPM cap / non-finite)
-  double pcg_bytes = 0.0;
-  if (lane < 8) F.cyc[lane] = 0;
-  __syncwarp();
-  long long tk = clock64();
-  for (int k = 0;; ++k) {
-    bool changed = cut_search(F, P);
-    if (!changed) break;
-    if (k == P.alp_max_iter) {
-      status |= ST_ALP_MAXITER;
-      break;
-    }
-    // Reading C-12: the LP (hence u^k and the next cut search) is a function of the pool, so
-    // a pool equal to that of an LP already solved repeats forever: stop with the last solved
-    // u (G2) and the cap status.  Pools are compared by a 64-bit order-independent hash.
-    {
-      unsigned long long hsh = 0ull;
-      for (int j = lane; j < m; j += 32) {
-        unsigned long long v = ((unsigned long long)(unsigned)j << 16) | F.mask[j];
-        v *= 0x9E3779B97F4A7C15ull;
-        v ^= v >> 29;
-        v *= 0xBF58476D1CE4E5B9ull;
-        v ^= v >> 32;
-        hsh += (F.mask[j] & PRESENT) ? v : 0ull;
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) hsh += __shfl_xor_sync(FULL, hsh, o);
-      bool seen = false;
-      for (int t = lane; t < k; t += 32) seen |= (F.hist[t] == hsh);
-      if (__any_sync(FULL, seen)) {
-        status |= ST_ALP_MAXITER;
-        break;
-      }
-      if (lane == 0) F.hist[k] = hsh;
-      __syncwarp();
-    }
-    int p, nact;
-    double bmax;
-    build_signs(F, true, p, nact, bmax);
-    ALP_TICK(F, CY_CUT, tk);
-    ++lp_solves;
-    max_p = max(max_p, p);
-    IpmOut o = ipm_solve(F, P, g, p, nact, bmax, cmax, f, lp_solves);
-    status |= o.status;
-    last_lp_bad = (o.status & (ST_IPM_MAXITER | ST_NUMERIC)) != 0;
-    ipm_iters += o.iters;
-    pcg_iters += o.pcg_iters;
-    pcg_bytes += o.pcg_bytes;
-    solves += o.solves;
-    p4_fail += o.p4_fail;
-    true_fail += o.true_fail;
-    max_rec = fmax(max_rec, o.max_rec);
-    max_true = fmax(max_true, o.max_true);
-    for (int i = lane; i < n; i += 32) {
-      double xi = F.x[i];
-      F.u[i] = F.flip[i] ? 1.0 - xi : xi;
-    }
-    __syncwarp();
-    tk = clock64();
-    // Reading C-30: an LP whose IPM ended on a non-finite iterate or at the Newton-step cap
-    // gives no trustworthy u for the next cut search, so the frame's decode stops there
-    // (status bits set, last u output; `stop_on_lp_failure = 0` keeps going).
-    if ((o.status & ST_NUMERIC) || (P.stop_on_lp_failure && (o.status & ST_IPM_MAXITER))) break;
-  }
-  ALP_TICK(F, CY_CUT, tk);
-  // outputs: hard decision, objective gamma^T u, g_max, ML certificate
-  double obj = 0.0, gm = 0.0;
-  for (int i = lane; i < n; i += 32) {
-    double ui = F.u[i];
-    obj += g[i] * ui;
-    gm = fmax(gm, fmin(ui, 1.0 - ui));
-    O.hard[f * n + i] = (ui > 0.5) ? 1 : 0;
-    if (O.u_out) O.u_out[f * n + i] = ui;
-  }
-  bool parity_bad = false;
-  for (int j = lane; j < m; j += 32) {
-    int deg = C.chk_deg[j];
-    int par = 0;
-    for (int t = 0; t < deg; ++t) par ^= (F.u[chk_nb(C, j, t)] > 0.5) ? 1 : 0;
-    parity_bad |= (par != 0);
-    uint16_t mk = F.mask[j];
-    if (O.y_out) O.y_out[f * m + j] = (mk & PRESENT) ? F.y[j] : 0.0;
-    if (O.mask_out) O.mask_out[f * m + j] = mk;
-  }
-  obj = wsum(obj);
-  gm = wmax(gm);
-  bool pbad = __any_sync(FULL, parity_bad);
-  if (lane == 0) {
-    O.objective[f] = obj;
-    // ML certificate (C-11): an integral codeword that is the optimum of the LP; an LP
-    // whose IPM did not converge proves nothing, so its u never certifies (C-31)
-    O.cert[f] = (gm <= P.tau_cert && !pbad && !last_lp_bad) ? 1 : 0;
-    if (O.status) O.status[f] = status;
-    if (O.stats) {
-      alp_frame_stats st;
-      st.lp_solves = lp_solves;
-      st.ipm_iters = ipm_iters;
-      st.pcg_iters = pcg_iters;
-      st.max_p = max_p;
-      st.pcg_solves = solves;
-      st.pcg_p4_fail = p4_fail;
-      st.pcg_true_fail = true_fail;
-      st.reserved = 0;
-      st.max_rec_relres = max_rec;
-      st.max_true_relres = max_true;
-      st.g_max = gm;
-      st.pcg_bytes = pcg_bytes;
-      st.cyc_cut = F.cyc[CY_CUT];
-      st.cyc_ipm = F.cyc[CY_IPM];
-      st.cyc_build = F.cyc[CY_BUILD];
-      st.cyc_spmv = F.cyc[CY_SPMV];
-      st.cyc_sweep = F.cyc[CY_SWEEP];
-      st.cyc_pcg_other = F.cyc[CY_PCG];
-      st.cyc_sort = F.cyc[CY_SORT];
-      st.cyc_peel = F.cyc[CY_PEEL];
-      O.stats[f] = st;
-    }
-  }
-  __syncwarp();
-}
-
-#ifndef ALP_MINB
-#define ALP_MINB 1
-#endif
-__global__ void __launch_bounds__(128, ALP_MINB) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
-                                                        char* slots,
-                                                        const double* __restrict__ llr,
-                                                        long long n_frames, DecodeOut O,
-                                                        unsigned long long* counter) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ DCode sC;    // code / layout descriptors in shared memory: the Frame's pointers to
-  __shared__ Layout sL;   // them must not land in local memory
-  if (threadIdx.x == 0) sL = L;
-  DCode Cs;
-  stage_graph(C, G, smem, Cs);
-  if (threadIdx.x == 0) sC = Cs;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
-  Frame F;
-  char* slot = slots + gw * L.slot_bytes;
-  frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
-  __shared__ long long s_cyc[4][8];   // phase clocks in shared memory (a global RMW per tick
-  F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
-  while (true) {
-    long long f = 0;
-    if (lane == 0) f = (long long)atomicAdd(counter, 1ull);   // 64-bit: no wrap at any n_frames
-    f = __shfl_sync(FULL, f, 0);
-    if (f >= n_frames) break;
-    decode_frame(F, P, llr + f * C.n, f, O);
-  }
-}
 
 struct StepIO {
   const uint16_t* masks;
@@ -485,64 +49,21 @@ struct StepIO {
   int* pcol;
 };
 
-// Isolated step solve (eq.`Delta y` P:479) per system: signs, D^2, Alg. 7, PCG.
-__global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout L, GraphSmem G,
-                                                      char* slots, long long n_sys, StepIO io,
-                                                      unsigned long long* counter) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ DCode sC;
-  __shared__ Layout sL;
-  if (threadIdx.x == 0) sL = L;
-  DCode Cs;
-  stage_graph(C, G, smem, Cs);
-  if (threadIdx.x == 0) sC = Cs;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
-  Frame F;
-  char* slot = slots + gw * L.slot_bytes;
-  frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
-  const int n = C.n, m = C.m, Q = C.Q;
-  while (true) {
-    long long s = 0;
-    if (lane == 0) s = (long long)atomicAdd(counter, 1ull);
-    s = __shfl_sync(FULL, s, 0);
-    if (s >= n_sys) break;
-    for (int j = lane; j < m; j += 32) F.mask[j] = io.masks[s * m + j];
-    for (int i = lane; i < n; i += 32) F.flip[i] = io.flip ? (io.flip[s * n + i] ? 1 : 0) : 0;
-    __syncwarp();
-    int p, nact;
-    double bmax;
-    build_signs(F, false, p, nact, bmax);
-    for (int c = lane; c < Q; c += 32) {
-      double dd = io.d[s * Q + c];
-      F.d2[c] = dd * dd;
-    }
-    for (int j = lane; j < m; j += 32) F.w[j] = (F.sgnC[j] & PRESENT) ? io.r[s * m + j] : 0.0;
-    __syncwarp();
-    int nLb = 0, nLf = 0;
-    const bool mtm = (P.precond == 0) && p > 0;
-    if (mtm) build_precond(F, p, nLb, nLf);
-    if ((io.prow || io.pcol)) {
-      if (mtm) write_pivots(F, p, io.prow ? io.prow + s * m : nullptr, io.pcol ? io.pcol + s * m : nullptr);
-      else
-        for (int k = lane; k < m; k += 32) {
-          if (io.prow) io.prow[s * m + k] = -1;
-          if (io.pcol) io.pcol[s * m + k] = -1;
-        }
-    }
-    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, P.pcg_rel_tol, true);
-    for (int j = lane; j < m; j += 32) io.dy[s * m + j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
-    if (lane == 0) {
-      if (io.iters) io.iters[s] = pr.iters;
-      if (io.relres) io.relres[s] = pr.relres;
-      if (io.status) io.status[s] = pr.status;
-    }
-    __syncwarp();
-  }
-}
-
 }  // namespace alp
+
+// The device code twice: shared-memory window (sm) and generic window (gm).
+#define ALP_NS sm
+#define ALP_SM 1
+#include "alp_device.cuh"
+#include "alp_kernels.cuh"
+#undef ALP_NS
+#undef ALP_SM
+#define ALP_NS gm
+#define ALP_SM 0
+#include "alp_device.cuh"
+#include "alp_kernels.cuh"
+#undef ALP_NS
+#undef ALP_SM
 
 // =====================================================================================
 // Host side
@@ -590,8 +111,8 @@ DCode make_dcode(const alp_code* c) {
   return C;
 }
 
-Layout make_layout(const DCode& C, int smem_budget) {
-  Layout L;
+// Per-frame global slot (both window modes); returns the byte count used so far.
+size_t make_slot(const DCode& C, Layout& L) {
   const size_t n = C.n, m = C.m, Q = C.Q;
   size_t o = 0;
   auto g = [&](size_t bytes) {
@@ -624,6 +145,87 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.g_rc = g(8 * Q);
   L.g_pcol = g(2 * m);
   L.slot_bytes = (long long)al(o, 256);
+  return o;
+}
+
+// Window layout of the shared-memory mode (kernel alp::sm::*): one fixed per-frame window,
+//   P: PCG vectors h, r, f, z [m] (t [n] over f, z when it fits, else after them); the build's
+//      late arrays (pos, pcol, prow, lvB, lvF, poc, hist, cur) overlay P;
+//   sgnC [m], sgnV [n];
+//   D: l, dy, dinvF [m], level offsets, sweep records (all dead while the preconditioner is
+//      being built); the build's early arrays (order, radix buffers / rank, cnt, xr, DEG1
+//      bitmap, row ranks) overlay D.
+// d^2, w and the IPM arrays stay in the slot (L1/L2).  Returns false when the late arrays do
+// not fit P (then the generic mode is used).
+bool make_layout_sm(const DCode& C, Layout& L) {
+  const size_t n = C.n, m = C.m, Q = C.Q;
+  make_slot(C, L);
+  L.win_global = 0;
+  L.g_win = 0;
+  size_t a = 0;
+  auto s = [&](size_t bytes) {
+    size_t r = a;
+    a += al(bytes, 16);
+    return (int)r;
+  };
+  // P
+  L.s_h = s(8 * m);
+  L.s_r = s(8 * m);
+  L.s_f = s(8 * m);
+  L.s_z = s(8 * m);
+  size_t endP = a;
+  if (8 * n <= endP - L.s_f) L.s_t = L.s_f;
+  else { L.s_t = s(8 * n); endP = a; }
+  a = 0;   // late build arrays over P
+  L.s_pos = s(2 * m);
+  L.s_pcol = s(2 * m);
+  L.s_prow = s(2 * m);
+  L.s_lvB = s(2 * m);
+  L.s_lvF = s(2 * m);
+  L.s_poc = s(2 * Q);
+  L.s_hist = s(4 * (m + 2));
+  L.s_cur = s(4 * (m + 2));
+  if (a > endP) return false;
+  a = endP;
+  L.smask = 0;
+  auto rel = [&](int k, size_t bytes) {
+    L.smask |= 1u << k;
+    L.soff[k] = s(bytes);
+  };
+  rel(RL_SGNC, 2 * m);
+  rel(RL_SGNV, n);
+  // D
+  const size_t D0 = a;
+  rel(RL_L, 8 * m);
+  rel(RL_DY, 8 * m);
+  rel(RL_DINVF, 8 * m);
+  rel(RL_OFFB, 4 * (m + 2));
+  rel(RL_OFFF, 4 * (m + 2));
+  rel(RL_RECF, 2 * m * (size_t)RF);
+  rel(RL_RECB, 2 * m * (size_t)C.RB);
+  size_t endD = a;
+  a = D0;   // early build arrays over D
+  L.s_order = s(2 * Q);
+  const size_t E0 = a;
+  L.s_sortk = (int)E0;
+  L.s_sorth = (int)(E0 + al(12 * Q, 16));
+  const size_t endSort = E0 + al(12 * Q, 16) + 2048;
+  a = E0;
+  L.s_rank = s(2 * Q);
+  L.s_cnt = s(Q);
+  L.s_xr = s(2 * Q);
+  L.s_bm = s(8 * (size_t)C.W);
+  L.RS = (C.dc + 1 <= 8) ? 8 : 16;
+  L.s_rrank = s(2 * m * (size_t)L.RS);
+  const size_t endE = std::max(a, endSort);
+  L.smem_bytes = (int)al(std::max(endD, endE), 128);
+  return true;
+}
+
+Layout make_layout(const DCode& C, int smem_budget) {
+  Layout L;
+  const size_t n = C.n, m = C.m, Q = C.Q;
+  size_t o = make_slot(C, L);
   // shared window
   size_t a = 0;
   auto s = [&](size_t bytes) {
@@ -837,6 +439,40 @@ alp_status plan_launch(K kernel, const Layout& L, int graph_bytes, long long uni
 
 const size_t kCounterBytes = 256;
 
+// Launch plan: the shared-memory window mode (alp::sm kernels, fixed layout, LDS everywhere)
+// when its per-frame window fits at least 2 frames per CTA and the caller did not ask for a
+// specific shared-memory split; otherwise the generic mode (alp::gm kernels, budget relocation,
+// global window for large codes).
+struct Plan {
+  bool sm;
+  Layout L;
+  GraphSmem G;
+  LaunchCfg cfg;
+};
+
+alp_status make_plan(const alp_code* code, int64_t units, const alp_params* p, bool step, Plan& pl) {
+  const DCode C = make_dcode(code);
+  pl.G = make_graph_smem(C);
+  units = std::max<int64_t>(units, 1);
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
+    optin = 227 * 1024;
+  const bool want_gm = p && p->smem_frames_per_sm > 0;
+  if (!want_gm && make_layout_sm(C, pl.L)) {
+    const int wpb = (p && p->warps_per_block > 0) ? p->warps_per_block : 4;
+    if ((long long)std::min(wpb, 2) * pl.L.smem_bytes + pl.G.bytes <= optin - 1024) {
+      pl.sm = true;
+      return step ? plan_launch(sm::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
+                  : plan_launch(sm::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
+    }
+  }
+  pl.sm = false;
+  pl.L = make_layout(C, smem_budget_for(p));
+  return step ? plan_launch(gm::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
+              : plan_launch(gm::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
+}
+
 }  // namespace
 
 extern "C" {
@@ -987,11 +623,9 @@ size_t alp_decode_workspace_bytes(const alp_code* code, int64_t n_frames, const 
     if (!code || n_frames < 0) fail(ALP_ERR_INVALID_ARG, "bad code or n_frames");
     return 0;
   }
-  DCode C = make_dcode(code);
-  Layout L = make_layout(C, smem_budget_for(params));
-  LaunchCfg cfg;
-  if (plan_launch(alp_decode_kernel, L, make_graph_smem(C).bytes, std::max<int64_t>(n_frames, 1), params, cfg) != ALP_OK) return 0;
-  return kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
+  Plan pl;
+  if (make_plan(code, n_frames, params, false, pl) != ALP_OK) return 0;
+  return kCounterBytes + (size_t)pl.cfg.slots * (size_t)pl.L.slot_bytes;
 }
 
 size_t alp_pcg_workspace_bytes(const alp_code* code, int64_t n_sys, const alp_params* params) {
@@ -1000,11 +634,9 @@ size_t alp_pcg_workspace_bytes(const alp_code* code, int64_t n_sys, const alp_pa
     if (!code || n_sys < 0) fail(ALP_ERR_INVALID_ARG, "bad code or n_sys");
     return 0;
   }
-  DCode C = make_dcode(code);
-  Layout L = make_layout(C, smem_budget_for(params));
-  LaunchCfg cfg;
-  if (plan_launch(pcg_step_kernel, L, make_graph_smem(C).bytes, std::max<int64_t>(n_sys, 1), params, cfg) != ALP_OK) return 0;
-  return kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
+  Plan pl;
+  if (make_plan(code, n_sys, params, true, pl) != ALP_OK) return 0;
+  return kCounterBytes + (size_t)pl.cfg.slots * (size_t)pl.L.slot_bytes;
 }
 
 alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr, uint8_t* hard,
@@ -1022,13 +654,11 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
     return fail(ALP_ERR_INVALID_ARG, "llr, hard, objective and certificate are required");
   if (!workspace || ((uintptr_t)workspace & 255))
     return fail(ALP_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
-  DCode C = make_dcode(code);
-  Layout L = make_layout(C, smem_budget_for(params));
-  LaunchCfg cfg;
-  const GraphSmem G = make_graph_smem(C);
-  alp_status st = plan_launch(alp_decode_kernel, L, G.bytes, n_frames, params, cfg);
+  const DCode C = make_dcode(code);
+  Plan pl;
+  alp_status st = make_plan(code, n_frames, params, false, pl);
   if (st != ALP_OK) return st;
-  size_t need = kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
+  size_t need = kCounterBytes + (size_t)pl.cfg.slots * (size_t)pl.L.slot_bytes;
   if (workspace_bytes < need)
     return fail(ALP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1036,8 +666,13 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(*counter), s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   DecodeOut O{hard, objective, certificate, frame_status, stats, u_out, y_out, mask_out};
-  alp_decode_kernel<<<cfg.grid, 32 * cfg.wpb, cfg.smem_block, s>>>(
-      C, make_params(params), L, G, (char*)workspace + kCounterBytes, llr, (long long)n_frames, O, counter);
+  char* slots = (char*)workspace + kCounterBytes;
+  if (pl.sm)
+    sm::alp_decode_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
+        C, make_params(params), pl.L, pl.G, slots, llr, (long long)n_frames, O, counter);
+  else
+    gm::alp_decode_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
+        C, make_params(params), pl.L, pl.G, slots, llr, (long long)n_frames, O, counter);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "alp_decode_kernel launch");
   g_last_launches = 1;
@@ -1114,13 +749,11 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   if (!masks || !d || !r || !dy) return fail(ALP_ERR_INVALID_ARG, "masks, d, r and dy are required");
   if (!workspace || ((uintptr_t)workspace & 255))
     return fail(ALP_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
-  DCode C = make_dcode(code);
-  Layout L = make_layout(C, smem_budget_for(params));
-  LaunchCfg cfg;
-  const GraphSmem G = make_graph_smem(C);
-  alp_status st = plan_launch(pcg_step_kernel, L, G.bytes, n_sys, params, cfg);
+  const DCode C = make_dcode(code);
+  Plan pl;
+  alp_status st = make_plan(code, n_sys, params, true, pl);
   if (st != ALP_OK) return st;
-  size_t need = kCounterBytes + (size_t)cfg.slots * (size_t)L.slot_bytes;
+  size_t need = kCounterBytes + (size_t)pl.cfg.slots * (size_t)pl.L.slot_bytes;
   if (workspace_bytes < need)
     return fail(ALP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1128,8 +761,13 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(*counter), s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   StepIO io{masks, flip, d, r, dy, pcg_iters, rel_res, sys_status, pivot_rows, pivot_cols};
-  pcg_step_kernel<<<cfg.grid, 32 * cfg.wpb, cfg.smem_block, s>>>(
-      C, make_params(params), L, G, (char*)workspace + kCounterBytes, (long long)n_sys, io, counter);
+  char* slots = (char*)workspace + kCounterBytes;
+  if (pl.sm)
+    sm::pcg_step_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
+        C, make_params(params), pl.L, pl.G, slots, (long long)n_sys, io, counter);
+  else
+    gm::pcg_step_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
+        C, make_params(params), pl.L, pl.G, slots, (long long)n_sys, io, counter);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pcg_step_kernel launch");
   g_last_launches = 1;

@@ -9,7 +9,6 @@
 // by whichever PCG-hot slot arrays fit the window budget (Layout::smask).  Each CTA stages the
 // Tanner graph and the code / layout descriptors in shared memory (stage_graph).
 // Citations: PAPER.md line numbers (P:n) with section / algorithm / equation label.
-#pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -20,7 +19,11 @@
 #define ALP_HEAVY
 #endif
 
+#ifndef ALP_DEVICE_TYPES
+#define ALP_DEVICE_TYPES
 namespace alp {
+
+extern __shared__ __align__(16) char alp_dsmem[];   // the kernels' dynamic shared memory
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint16_t PRESENT = 0x8000u;
@@ -137,6 +140,44 @@ enum { CY_CUT = 0, CY_IPM = 1, CY_BUILD = 2, CY_SPMV = 3, CY_SWEEP = 4, CY_PCG =
     (t) = now_;                                     \
   } while (0)
 
+enum { RL_SGNC = 0, RL_SGNV, RL_L, RL_DY, RL_DINVF, RL_OFFB, RL_OFFF, RL_RECF, RL_RECB, RL_D2, RL_W,
+       RL_N };
+
+__device__ __forceinline__ char* rel_ptr(const Layout* L, char* slot, char* sm, int k, long long g) {
+  return ((L->smask >> k) & 1u) ? sm + L->soff[k] : slot + g;
+}
+
+__device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
+  const unsigned v = C.chk_var[j * C.dc + t];
+  return v == 0xffffu ? -1 : (int)v;
+}
+__device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
+  const unsigned v = C.var_chk[i * C.dv + k];
+  return v == 0xffffu ? -1 : (int)v;
+}
+
+}  // namespace alp
+#endif  // ALP_DEVICE_TYPES
+
+// ---------------------------------------------------------------------------------------------
+// Mode-dependent device code, included once per window mode (alp.cu):
+//   ALP_NS = sm, ALP_SM = 1: the whole per-frame window and the PCG-hot arrays live in shared
+//     memory (fixed layout, make_layout_sm); ALP_SH(p) tells the compiler so, and the loads are
+//     LDS instead of generic loads (measured: generic loads dominated the stalls, ncu r2a).
+//   ALP_NS = gm, ALP_SM = 0: budget-relocated arrays, possibly a global-memory window (large
+//     codes, e.g. config 4); every access is a generic load.
+// ---------------------------------------------------------------------------------------------
+#define ALP_SH(p) ((void)0)
+#define ALP_GL_SM(p) ((void)0)
+#define ALP_GL(p) ((void)0)
+#ifdef ALP_ASSUME_S_ONLY
+#define ALP_SHA(p) ((void)0)
+#else
+#define ALP_SHA(p) ALP_SH(p)
+#endif   // (an __isGlobal assume broke the NVVM module; generic loads stay)
+namespace alp {
+namespace ALP_NS {
+
 // Per-frame working set: pointers into the warp's global slot and shared window.
 struct Frame {
   const DCode* C;
@@ -153,16 +194,39 @@ struct Frame {
   uint8_t* sgnV;   // [n]: bit k <-> k-th check of the variable present; bit 4+k <-> coef -1
   uint8_t* flip;   // [n]: 1 <-> gamma_i < 0 (x_i = 1 - u_i, §IV-B)
   long long* cyc;  // [8] per-phase clock64 accumulators (lane 0 writes; alp_frame_stats)
+#if ALP_SM
+  // sm mode: every window / relocated address is formed from the dynamic shared-memory
+  // symbol itself, so the compiler emits LDS/STS (a generic pointer kept in the Frame would
+  // compile to generic loads).  smo = the frame window's byte offset in dynamic shared memory.
+  unsigned smo;
+  unsigned o_sgnC, o_sgnV, o_l, o_dy, o_dinvF, o_recB, o_recF, o_offB, o_offF;
+  template <class T>
+  __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(alp_dsmem + smo + off); }
+  template <class T>
+  __device__ __forceinline__ T* W_(unsigned off) const { return reinterpret_cast<T*>(alp_dsmem + smo + off); }
+  __device__ __forceinline__ uint16_t* sgnC_() const { return W_<uint16_t>(o_sgnC); }
+  __device__ __forceinline__ uint8_t* sgnV_() const { return W_<uint8_t>(o_sgnV); }
+  __device__ __forceinline__ double* l_() const { return W_<double>(o_l); }
+  __device__ __forceinline__ double* dy_() const { return W_<double>(o_dy); }
+  __device__ __forceinline__ double* dinvF_() const { return W_<double>(o_dinvF); }
+  __device__ __forceinline__ uint16_t* recB_() const { return W_<uint16_t>(o_recB); }
+  __device__ __forceinline__ uint16_t* recF_() const { return W_<uint16_t>(o_recF); }
+  __device__ __forceinline__ int* offB_() const { return W_<int>(o_offB); }
+  __device__ __forceinline__ int* offF_() const { return W_<int>(o_offF); }
+#else
   template <class T>
   __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(sm + off); }
+  __device__ __forceinline__ uint16_t* sgnC_() const { return sgnC; }
+  __device__ __forceinline__ uint8_t* sgnV_() const { return sgnV; }
+  __device__ __forceinline__ double* l_() const { return l; }
+  __device__ __forceinline__ double* dy_() const { return dy; }
+  __device__ __forceinline__ double* dinvF_() const { return dinvF; }
+  __device__ __forceinline__ uint16_t* recB_() const { return recB; }
+  __device__ __forceinline__ uint16_t* recF_() const { return recF; }
+  __device__ __forceinline__ int* offB_() const { return offB; }
+  __device__ __forceinline__ int* offF_() const { return offF; }
+#endif
 };
-
-enum { RL_SGNC = 0, RL_SGNV, RL_L, RL_DY, RL_DINVF, RL_OFFB, RL_OFFF, RL_RECF, RL_RECB, RL_D2, RL_W,
-       RL_N };
-
-__device__ __forceinline__ char* rel_ptr(const Layout* L, char* slot, char* sm, int k, long long g) {
-  return ((L->smask >> k) & 1u) ? sm + L->soff[k] : slot + g;
-}
 
 __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layout* L, char* slot,
                                            char* sm, int lane) {
@@ -192,6 +256,30 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.rb = (double*)(slot + L->g_rb);
   F.rc = (double*)(slot + L->g_rc);
   F.pcolR = (uint16_t*)(slot + L->g_pcol);
+#if ALP_SM
+  // sm mode: the PCG-hot arrays are always in the window (make_layout_sm), d^2 and w never
+  F.smo = (unsigned)(sm - alp_dsmem);
+  F.o_sgnC = L->soff[RL_SGNC];
+  F.o_sgnV = L->soff[RL_SGNV];
+  F.o_l = L->soff[RL_L];
+  F.o_dy = L->soff[RL_DY];
+  F.o_dinvF = L->soff[RL_DINVF];
+  F.o_recB = L->soff[RL_RECB];
+  F.o_recF = L->soff[RL_RECF];
+  F.o_offB = L->soff[RL_OFFB];
+  F.o_offF = L->soff[RL_OFFF];
+  F.sgnC = F.sgnC_();
+  F.sgnV = F.sgnV_();
+  F.l = F.l_();
+  F.dy = F.dy_();
+  F.dinvF = F.dinvF_();
+  F.recB = F.recB_();
+  F.recF = F.recF_();
+  F.offB = F.offB_();
+  F.offF = F.offF_();
+  F.flip = (uint8_t*)(slot + L->g_flip);
+  return;
+#endif
   F.recB = (uint16_t*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
   F.recF = (uint16_t*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
   F.offB = (int*)rel_ptr(L, slot, sm, RL_OFFB, L->g_offB);
@@ -204,15 +292,6 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.dy = (double*)rel_ptr(L, slot, sm, RL_DY, L->g_dy);
   F.w = (double*)rel_ptr(L, slot, sm, RL_W, L->g_w);
   F.flip = (uint8_t*)(slot + L->g_flip);
-}
-
-__device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
-  const unsigned v = C.chk_var[j * C.dc + t];
-  return v == 0xffffu ? -1 : (int)v;
-}
-__device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
-  const unsigned v = C.var_chk[i * C.dv + k];
-  return v == 0xffffu ? -1 : (int)v;
 }
 
 // =====================================================================================
@@ -250,7 +329,7 @@ __device__ ALP_HEAVY void build_signs(const Frame& F, bool want_b, int& p_out, i
         bmax = fmax(bmax, fabs(bj));
       }
     }
-    F.sgnC[j] = s;
+    F.sgnC_()[j] = s;
   }
   __syncwarp();
   int nact = 0;
@@ -260,13 +339,13 @@ __device__ ALP_HEAVY void build_signs(const Frame& F, bool want_b, int& p_out, i
     for (int k = 0; k < dv; ++k) {
       int j = var_ck(C, i, k);
       int t = C.var_slot[i * C.dv + k];
-      uint16_t sc = F.sgnC[j];
+      uint16_t sc = F.sgnC_()[j];
       if (sc & PRESENT) {
         s |= (uint8_t)(1u << k);
         if ((sc >> t) & 1) s |= (uint8_t)(1u << (4 + k));
       }
     }
-    F.sgnV[i] = s;
+    F.sgnV_()[i] = s;
     nact += (s & 0xf) ? 1 : 0;
   }
   p_out = wsumi(p);
@@ -345,9 +424,10 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
 __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
-  const uint16_t* __restrict__ sgnC = F.sgnC;
-  const uint8_t* __restrict__ sgnV = F.sgnV;
+  const uint16_t* __restrict__ sgnC = F.sgnC_();
+  const uint8_t* __restrict__ sgnV = F.sgnV_();
   const double* __restrict__ d2 = F.d2;
+  ALP_GL_SM(d2);
   uint32_t* kA = F.S<uint32_t>(L.s_sortk);
   uint32_t* kB = kA + C.Q;
   uint16_t* cA = reinterpret_cast<uint16_t*>(kB + C.Q);
@@ -606,7 +686,7 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
     if (rk == (int)NONE16) continue;   // no present row (C-10): never in DEG1
     int cn = 0, x = 0;
     if (c < C.n) {
-      uint8_t s = F.sgnV[c];
+      uint8_t s = F.sgnV_()[c];
       int dv = C.var_deg[c];
       for (int k = 0; k < dv; ++k)
         if ((s >> k) & 1) {
@@ -622,7 +702,7 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
     if (cn == 1) atomicOr(&bm[rk >> 6], 1ull << (rk & 63));
   }
   for (int R = F.lane; R < C.m; R += 32) {
-    if (!(F.sgnC[R] & PRESENT)) continue;
+    if (!(F.sgnC_()[R] & PRESENT)) continue;
     const int deg = C.chk_deg[R];
     for (int t = 0; t < RS; ++t)
       rrank[R * RS + t] = (t < deg) ? rank[chk_nb(C, R, t)] : (t == deg ? rank[C.n + R] : NONE16);
@@ -643,7 +723,7 @@ __device__ __forceinline__ int back_deps(const Frame& F, int R, int* deps) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const uint16_t* poc = F.S<uint16_t>(F.L->s_poc);
   int deg = C.chk_deg[R];
-  uint16_t s = F.sgnC[R];
+  uint16_t s = F.sgnC_()[R];
   int pc = F.S<uint16_t>(F.L->s_pcol)[R];
   int nd = 0;
   for (int t = 0; t < deg; ++t) {
@@ -659,7 +739,7 @@ __device__ __forceinline__ int fwd_deps(const Frame& F, int R, int* deps) {
   int c = F.S<uint16_t>(F.L->s_pcol)[R];
   int nd = 0;
   if (c < C.n) {
-    uint8_t s = F.sgnV[c];
+    uint8_t s = F.sgnV_()[c];
     int dv = C.var_deg[c];
     for (int k = 0; k < dv; ++k) {
       if (!((s >> k) & 1)) continue;
@@ -675,7 +755,7 @@ __device__ __forceinline__ int diag_neg(const Frame& F, int R) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   int c = F.S<uint16_t>(F.L->s_pcol)[R];
   if (c >= C.n) return 0;
-  uint8_t s = F.sgnV[c];
+  uint8_t s = F.sgnV_()[c];
   int dv = C.var_deg[c];
   for (int k = 0; k < dv; ++k)
     if (var_ck(C, c, k) == R) return (s >> (4 + k)) & 1;
@@ -803,8 +883,8 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
   uint16_t* lvF = F.S<uint16_t>(L.s_lvF);
   nLb = compute_levels<false>(F, p, lvB);
   nLf = compute_levels<true>(F, p, lvF);
-  level_slots(F, p, nLb, lvB, F.offB);
-  level_slots(F, p, nLf, lvF, F.offF);
+  level_slots(F, p, nLb, lvB, F.offB_());
+  level_slots(F, p, nLf, lvF, F.offF_());
   // Records (u16, rows < 32768): word 0 = R | diag_neg << 15, then the dependencies
   // (row | coefficient_neg << 15), unused slots NODEP.  Back: RB words (8 or 16) per pivot,
   // forward: RF = 4 words per pivot (d_v <= 4) + dinvF = 1 / d^2 of the pivot column.
@@ -813,15 +893,15 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
     int deps[DCMAX];
     const int dn = diag_neg(F, R);
     int nd = back_deps(F, R, deps);
-    uint16_t* rb = F.recB + (size_t)lvB[k] * C.RB;
+    uint16_t* rb = F.recB_() + (size_t)lvB[k] * C.RB;
     rb[0] = (uint16_t)(R | (dn << 15));
     for (int d = 1; d < C.RB; ++d) rb[d] = (d <= nd) ? (uint16_t)((deps[d - 1] & 0x7fff) | ((deps[d - 1] < 0) << 15)) : NODEP;
     nd = fwd_deps(F, R, deps);
     const int sf = lvF[k];
-    uint16_t* rf = F.recF + (size_t)sf * RF;
+    uint16_t* rf = F.recF_() + (size_t)sf * RF;
     rf[0] = (uint16_t)(R | (dn << 15));
     for (int d = 1; d < RF; ++d) rf[d] = (d <= nd) ? (uint16_t)((deps[d - 1] & 0x7fff) | ((deps[d - 1] < 0) << 15)) : NODEP;
-    F.dinvF[sf] = 1.0 / F.d2[pcol[R]];
+    F.dinvF_()[sf] = 1.0 / F.d2[pcol[R]];
   }
   __syncwarp();
 }
@@ -845,7 +925,7 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 //                         + d2_{n+j} h_j (per check)                   [eq.`Delta y` LHS]
 //   M^-1 r: back sweep A_M f = r, scale by D_M^-2, forward sweep A_M^T z = f
 // Stops after line 9 once ||r||_2 <= tol ||w||_2 (G15).  h^T l <= 0 -> breakdown.
-// w is read from F.w; the solution accumulates in F.dy.
+// w is read from F.w; the solution accumulates in F.dy_().
 // =====================================================================================
 // Sweep records are read as int4 vectors; each level's first 32-slot chunk is prefetched
 // during the previous level (offsets and records do not depend on the values being
@@ -894,9 +974,9 @@ __device__ __forceinline__ void back_sweep_t(const Frame& F, int nLb) {
   const Layout& L = *F.L;
   const double* rS = F.S<double>(L.s_r);
   double* fS = F.S<double>(L.s_f);
-  const uint4* rec = reinterpret_cast<const uint4*>(F.recB);
+  const uint4* rec = reinterpret_cast<const uint4*>(F.recB_());
   OffReg off;
-  off.load(F.offB, nLb, F.lane);
+  off.load(F.offB_(), nLb, F.lane);
   int a = off(0), b = off(1);
   uint4 cur[RBW];
   bool hc = a + F.lane < b;
@@ -962,12 +1042,12 @@ __device__ ALP_HEAVY double fwd_sweep(const Frame& F, int nLf) {
   const Layout& L = *F.L;
   const double* fS = F.S<double>(L.s_f);
   double* zS = F.S<double>(L.s_z);
-  const uint2* __restrict__ recF = reinterpret_cast<const uint2*>(F.recF);   // RF == 4 u16
-  const double* __restrict__ dinvF = F.dinvF;
+  const uint2* __restrict__ recF = reinterpret_cast<const uint2*>(F.recF_());   // RF == 4 u16
+  const double* __restrict__ dinvF = F.dinvF_();
   double rz = 0.0;
   if (nLf <= 0) return rz;
   OffReg off;
-  off.load(F.offF, nLf, F.lane);
+  off.load(F.offF_(), nLf, F.lane);
   int a = off(0), b = off(1);
   uint2 cur = make_uint2(0u, 0u);
   double dcur = 0.0;
@@ -1037,11 +1117,12 @@ struct PcgResult {
 template <bool ABS, int DCT>
 __device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, const double* __restrict__ hS,
                                               const double* __restrict__ tS) {
-  const uint16_t* __restrict__ sgnC = F.sgnC;
+  const uint16_t* __restrict__ sgnC = F.sgnC_();
   const uint16_t* __restrict__ chk_var = C.chk_var;
   const uint8_t* __restrict__ chk_deg = C.chk_deg;
   const double* __restrict__ d2s_ = F.d2 + C.n;
-  double* __restrict__ lout = F.l;
+  ALP_GL_SM(d2s_);
+  double* __restrict__ lout = F.l_();
   const int m = C.m, dc = C.dc;
   double hl = 0.0;
   for (int j0 = F.lane; j0 < m; j0 += 64) {
@@ -1089,9 +1170,10 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
   const Layout& L = *F.L;
   const double* __restrict__ hS = F.S<double>(L.s_h);
   double* __restrict__ tS = F.S<double>(L.s_t);
-  const uint8_t* __restrict__ sgnV = F.sgnV;
+  const uint8_t* __restrict__ sgnV = F.sgnV_();
   const uint16_t* __restrict__ var_chk = C.var_chk;
   const double* __restrict__ d2 = F.d2;
+  ALP_GL_SM(d2);
   const int n = C.n, dvm = C.dv;
   const int dcs = C.dc;
   double hl = 0.0;
@@ -1176,18 +1258,18 @@ __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   double acc = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
-    const uint16_t sc = F.sgnC[j];
+    const uint16_t sc = F.sgnC_()[j];
     double r = 0.0;
     if (sc & PRESENT) {
-      DD l = dd_mul(DD{F.dy[j], 0.0}, F.d2[C.n + j]);
+      DD l = dd_mul(DD{F.dy_()[j], 0.0}, F.d2[C.n + j]);
       const int deg = C.chk_deg[j];
       for (int t = 0; t < deg; ++t) {
         const int i = chk_nb(C, j, t);
-        const uint8_t sv = F.sgnV[i];
+        const uint8_t sv = F.sgnV_()[i];
         DD ti{0.0, 0.0};
         for (int k = 0; k < C.var_deg[i]; ++k) {
           if (!((sv >> k) & 1)) continue;
-          const double h = F.dy[var_ck(C, i, k)];
+          const double h = F.dy_()[var_ck(C, i, k)];
           ti = dd_add(ti, ((sv >> (4 + k)) & 1) ? -h : h);
         }
         DD ui = dd_mul(ti, F.d2[i]);
@@ -1217,7 +1299,7 @@ __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
 // longer halves it within 1e3x of the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| ||
 // stops with ST_PCG_FLOOR (attainable accuracy, informational).
 // Status: 0 = the last recursion met pcg_rel_tol (P4), ST_PCG_MAXITER (cap or stall),
-// ST_PCG_BREAKDOWN, ST_PCG_FLOOR (refine mode).  w is read from F.w; dy accumulates in F.dy.
+// ST_PCG_BREAKDOWN, ST_PCG_FLOOR (refine mode).  w is read from F.w; dy accumulates in F.dy_().
 __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mode, int nLb, int nLf,
                                          double itol_rel, bool refine) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
@@ -1228,11 +1310,11 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
   double* fS = F.S<double>(L.s_f);
   double ww = 0.0;
   for (int j = F.lane; j < C.m; j += 32) {
-    const bool pr = (F.sgnC[j] & PRESENT) != 0;
+    const bool pr = (F.sgnC_()[j] & PRESENT) != 0;
     const double wj = pr ? F.w[j] : 0.0;
     ww += wj * wj;
     rS[j] = wj;        // lines 1-2: x^0 = 0, r^0 = w
-    F.dy[j] = 0.0;
+    F.dy_()[j] = 0.0;
     zS[j] = 0.0;       // absent rows stay exactly 0 in z, f and h (C-19)
     fS[j] = 0.0;
   }
@@ -1252,7 +1334,7 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
       res.status = ST_PCG_BREAKDOWN;
       break;
     }
-    for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? zS[j] : 0.0;   // line 4
+    for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC_()[j] & PRESENT) ? zS[j] : 0.0;   // line 4
     __syncwarp();
     int st = ST_PCG_MAXITER, past = -1, since_min = 0;
     double rrmin = 1e308, rr = 0.0;
@@ -1269,9 +1351,9 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
       const double alpha = rz / hl;   // line 7
       double acc = 0.0;
       {
-        double* __restrict__ dyp = F.dy;
-        const double* __restrict__ lp = F.l;
-        const uint16_t* __restrict__ sc = F.sgnC;
+        double* __restrict__ dyp = F.dy_();
+        const double* __restrict__ lp = F.l_();
+        const uint16_t* __restrict__ sc = F.sgnC_();
 #pragma unroll 4
         for (int j = F.lane; j < C.m; j += 32) {
           if (!(sc[j] & PRESENT)) continue;
@@ -1314,7 +1396,7 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
       const double nu = rz_new / rz;   // line 11
       rz = rz_new;
       {
-        const uint16_t* __restrict__ sc = F.sgnC;
+        const uint16_t* __restrict__ sc = F.sgnC_();
 #pragma unroll 4
         for (int j = F.lane; j < C.m; j += 32) {
           if (!(sc[j] & PRESENT)) continue;
@@ -1332,13 +1414,13 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
     if (refine) {
       trn = sqrt(residual_dd(F, rS));
     } else {
-      for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC[j] & PRESENT) ? F.dy[j] : 0.0;
+      for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC_()[j] & PRESENT) ? F.dy_()[j] : 0.0;
       __syncwarp();
       spmv<false>(F);
       double tr = 0.0;
       for (int j = F.lane; j < C.m; j += 32) {
         double r = 0.0;
-        if (F.sgnC[j] & PRESENT) r = F.w[j] - F.l[j];
+        if (F.sgnC_()[j] & PRESENT) r = F.w[j] - F.l_()[j];
         rS[j] = r;
         tr += r * r;
       }
@@ -1358,16 +1440,16 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
     double dn = 0.0, yn = 0.0;
     if (restart > 0) {
       for (int j = F.lane; j < C.m; j += 32) {
-        const double d = F.dy[j] - F.v[j];
+        const double d = F.dy_()[j] - F.v[j];
         dn += d * d;
-        yn += F.dy[j] * F.dy[j];
+        yn += F.dy_()[j] * F.dy_()[j];
       }
       dn = sqrt(wsum(dn));
       yn = sqrt(wsum(yn));
     }
     if (restart > 0 && st != 0) {
       // a refinement restart that did not converge: keep dy from before it (the last good one)
-      for (int j = F.lane; j < C.m; j += 32) F.dy[j] = F.v[j];
+      for (int j = F.lane; j < C.m; j += 32) F.dy_()[j] = F.v[j];
       __syncwarp();
       res.status = (res.relres_prev > P.pcg_rel_tol) ? ST_PCG_FLOOR : 0;
       res.relres = res.relres_prev;
@@ -1379,7 +1461,7 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
     }
     res.relres_prev = res.relres;
     if (restart > 0) prev_trn = dn;
-    for (int j = F.lane; j < C.m; j += 32) F.v[j] = F.dy[j];   // dy before the next correction
+    for (int j = F.lane; j < C.m; j += 32) F.v[j] = F.dy_()[j];   // dy before the next correction
     __syncwarp();
     itol = 1e-6 * trn;
   }
@@ -1387,4 +1469,5 @@ __device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mo
   return res;
 }
 
+}  // namespace ALP_NS
 }  // namespace alp

@@ -1,0 +1,515 @@
+// alp_kernels.cuh — IPM, frame decode and the two persistent kernels (included once per window
+// mode by alp.cu, inside namespace alp::ALP_NS; see alp_device.cuh).
+namespace alp {
+namespace ALP_NS {
+
+struct IpmOut {
+  int iters, status, pcg_iters, solves, p4_fail, true_fail;
+  double pcg_bytes, max_rec, max_true;
+};
+
+// =====================================================================================
+// Infeasible primal-dual path-following IPM (§IV-B) on the current pool LP
+// min c^T x, A x = b, x >= 0 (q = n + p columns; absent slack columns excluded).
+// Start x = z = s0 e, y = 0, s0 = max(1, ||b||, ||c||) (C-7).  Per iteration:
+// r_b = b - A x, r_c = c - A^T y - z, gap = x^T z; stop per C-8; mu = sigma gap / q
+// (eq.`update mu`, C-5); D^2 = X Z^-1, r_e = mu e - XZe; w = r_b + A (D^2 r_c - Z^-1 r_e)
+// (eq.`Delta y`); PCG for dy; dx = D^2 A^T dy - D^2 r_c + Z^-1 r_e (eq.`Delta x`);
+// dz = X^-1 (r_e - Z dx) (eq.`Delta z`); ratio test with eta (C-6); update.
+// Arrays: v holds r_c then D^2 r_c - Z^-1 r_e then dx; d2 holds D^2 then dz; w holds r_b
+// then the PCG right-hand side.
+// =====================================================================================
+__device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
+                            double bmax, double cmax, long long frame_id, int lp_id) {
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
+  const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
+  const double q = (double)(n + p);
+  // restrict-qualified views: the arrays never alias, which lets the unrolled loops below
+  // issue the next lane-iterations' loads before this one's stores
+  double* __restrict__ X = F.x;
+  double* __restrict__ Z = F.z;
+  double* __restrict__ Y = F.y;
+  double* __restrict__ V = F.v;
+  const double* __restrict__ B = F.b;
+  // (d2, w and dy are shared with build_precond / pcg_solve: plain pointers)
+  double* D2 = F.d2;
+  double* W = F.w;
+  const double* DY = F.dy_();
+  const uint16_t* __restrict__ SC = F.sgnC_();
+  const uint8_t* __restrict__ SV = F.sgnV_();
+  double* __restrict__ RBv = F.rb;   // r_b and r_c of the current iterate (kept for the recovery)
+  double* __restrict__ RCv = F.rc;
+  ALP_GL(X);
+  ALP_GL(Z);
+  ALP_GL(Y);
+  ALP_GL(V);
+  ALP_GL(B);
+  ALP_GL(RBv);
+  ALP_GL(RCv);
+  ALP_GL_SM(D2);
+  ALP_GL_SM(W);
+  const double s0 = fmax(1.0, fmax(bmax, cmax));
+  for (int c = lane; c < Q; c += 32) {
+    bool valid = (c < n) || (SC[c - n] & PRESENT);
+    X[c] = valid ? s0 : 0.0;
+    Z[c] = valid ? s0 : 0.0;
+  }
+  for (int j = lane; j < m; j += 32) Y[j] = 0.0;
+  __syncwarp();
+  IpmOut out{0, 0, 0, 0, 0, 0, 0.0, 0.0, 0.0};
+  long long tk = clock64();
+  // algorithmic bytes per PCG iteration of this LP
+  const double Bmin = 8.0 * (nact + p) + 48.0 * p + 5.0 * p + 2.0 * m;
+  int it = 0;
+  while (true) {
+    double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
+#pragma unroll 4
+    for (int j = lane; j < m; j += 32) {
+      uint16_t s = SC[j];
+      if (!(s & PRESENT)) continue;
+      int deg = C.chk_deg[j];
+      double acc = B[j] - X[n + j];
+      for (int t = 0; t < deg; ++t) {
+        double xi = X[chk_nb(C, j, t)];
+        acc = ((s >> t) & 1) ? acc + xi : acc - xi;
+      }
+      W[j] = acc;
+      RBv[j] = acc;
+      rbn = fmax(rbn, fabs(acc));
+      double rc = -Y[j] - Z[n + j];
+      V[n + j] = rc;
+      RCv[n + j] = rc;
+      rcn = fmax(rcn, fabs(rc));
+      gap += X[n + j] * Z[n + j];
+    }
+#pragma unroll 4
+    for (int i = lane; i < n; i += 32) {
+      double ci = fabs(g[i]);
+      uint8_t s = SV[i];
+      int dv = C.var_deg[i];
+      double acc = ci - Z[i];
+      for (int k = 0; k < dv; ++k) {
+        if (!((s >> k) & 1)) continue;
+        double yj = Y[var_ck(C, i, k)];
+        acc = ((s >> (4 + k)) & 1) ? acc + yj : acc - yj;
+      }
+      V[i] = acc;
+      RCv[i] = acc;
+      rcn = fmax(rcn, fabs(acc));
+      double xi = X[i];
+      gap += xi * Z[i];
+      cx += ci * xi;
+    }
+    __syncwarp();
+    rbn = wmax(rbn);
+    rcn = wmax(rcn);
+    gap = wsum(gap);
+    cx = wsum(cx);
+    if (gap <= P.gap_tol * (1.0 + fabs(cx)) && rbn <= P.feas_tol * (1.0 + bmax) &&
+        rcn <= P.feas_tol * (1.0 + cmax))
+      break;
+    if (it >= P.ipm_max_iter) {
+      out.status |= ST_IPM_MAXITER;
+      break;
+    }
+    const double mu = P.sigma * gap / q;
+#pragma unroll 4
+    for (int c = lane; c < Q; c += 32) {
+      if (c >= n && !(SC[c - n] & PRESENT)) continue;
+      double xc = X[c], zc = Z[c];
+      const double iz = 1.0 / zc;   // one division for D^2 = X Z^-1 and Z^-1 r_e
+      double d2 = xc * iz;
+      double re = mu - xc * zc;
+      D2[c] = d2;
+      V[c] = d2 * V[c] - re * iz;
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int j = lane; j < m; j += 32) {
+      uint16_t s = SC[j];
+      if (!(s & PRESENT)) continue;
+      int deg = C.chk_deg[j];
+      double acc = W[j] + V[n + j];
+      for (int t = 0; t < deg; ++t) {
+        double vi = V[chk_nb(C, j, t)];
+        acc = ((s >> t) & 1) ? acc - vi : acc + vi;
+      }
+      W[j] = acc;
+    }
+    __syncwarp();
+    int nLb = 0, nLf = 0;
+    const bool mtm = (P.precond == 0);
+    ALP_TICK(F, CY_IPM, tk);
+    // the Alg. 7 triangular set is both the PCG preconditioner (precond = 0) and the basis of
+    // the step's feasibility correction (C-32), so plain CG builds it too when that is on
+    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf);
+    ALP_TICK(F, CY_BUILD, tk);
+    // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to well
+    // below z ~ mu on the basic columns, so late in the IPM the recursion aims at
+    // min(pcg_rel_tol, 1e-2 mu) (floored at 1e-14); P4 acceptance is pcg_rel_tol.  An inexact
+    // dy is admissible because the recovery below keeps every KKT row but the complementarity
+    // of the basis columns exact (C-32).
+    const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, P.pcg_forcing * mu));
+    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, inner, false);
+    tk = clock64();
+    out.status |= pr.status;
+    out.solves += 1;
+    out.p4_fail += (pr.status != 0) ? 1 : 0;
+    out.true_fail += (pr.relres > P.pcg_rel_tol) ? 1 : 0;
+    out.max_rec = fmax(out.max_rec, pr.rec_relres);
+    out.max_true = fmax(out.max_true, pr.relres);
+    double dmn = 1e308, dmx = 0.0;
+    if (g_trace) {
+      for (int c = lane; c < Q; c += 32) {
+        if (c >= n && !(SC[c - n] & PRESENT)) continue;
+        dmn = fmin(dmn, D2[c]);
+        dmx = fmax(dmx, D2[c]);
+      }
+      dmn = wmin(dmn);
+      dmx = wmax(dmx);
+    }
+    out.pcg_iters += pr.iters;
+    out.pcg_bytes += (double)pr.iters * Bmin;
+    // Newton recovery (eq.`Delta x`, eq.`Delta z` P:480-481).  dz is taken in the algebraically
+    // identical form dz = r_c - A^T dy (eliminate dx from eq.`Delta z`), which keeps the dual
+    // equation A^T(y+dy) + z + dz = c exact for ANY dy; with dx from eq.`Delta x` the
+    // complementarity row Z dx + X dz = r_e is then exact too, so an inexact PCG dy only leaves
+    // the primal row off by the step residual rho = r_b - A dx = w - Q dy.  That residual is
+    // moved onto the preconditioner's basis columns: A_M f = rho (the back sweep of P:585),
+    // dx_M += f, so A dx = r_b holds to rounding (reading C-32; R-1).
+#pragma unroll 4
+    for (int i = lane; i < n; i += 32) {
+      uint8_t s = SV[i];
+      int dv = C.var_deg[i];
+      double atdy = 0.0;
+      for (int k = 0; k < dv; ++k) {
+        if (!((s >> k) & 1)) continue;
+        double d = DY[var_ck(C, i, k)];
+        atdy = ((s >> (4 + k)) & 1) ? atdy - d : atdy + d;
+      }
+      const double dx = D2[i] * atdy - V[i];
+      V[i] = dx;
+      D2[i] = RCv[i] - atdy;   // dz
+    }
+    for (int j = lane; j < m; j += 32) {
+      if (!(SC[j] & PRESENT)) continue;
+      const int c = n + j;
+      const double dx = D2[c] * DY[j] - V[c];
+      V[c] = dx;
+      D2[c] = RCv[c] - DY[j];
+    }
+    __syncwarp();
+    if (P.basis_correction && nLb > 0) {
+      double* rS = F.S<double>(F.L->s_r);
+      const double* fS = F.S<double>(F.L->s_f);
+      for (int j = lane; j < m; j += 32) {
+        uint16_t s = SC[j];
+        double rho = 0.0;
+        if (s & PRESENT) {
+          int deg = C.chk_deg[j];
+          double acc = RBv[j] - V[n + j];
+          for (int t = 0; t < deg; ++t) {
+            double xi = V[chk_nb(C, j, t)];
+            acc = ((s >> t) & 1) ? acc + xi : acc - xi;
+          }
+          rho = acc;
+        }
+        rS[j] = rho;
+      }
+      __syncwarp();
+      back_sweep(F, nLb);   // f = A_M^-1 rho, f_R = component of row R's pivot column
+      __syncwarp();
+      for (int j = lane; j < m; j += 32) {
+        const uint16_t c = F.pcolR[j];
+        if (c != NONE16) V[c] += fS[j];
+      }
+      __syncwarp();
+    }
+    // ratio test (C-6)
+    double ax = 1e308, az = 1e308;
+#pragma unroll 4
+    for (int c = lane; c < Q; c += 32) {
+      if (c >= n && !(SC[c - n] & PRESENT)) continue;
+      const double dx = V[c], dz = D2[c];
+      if (dx < 0.0) ax = fmin(ax, -X[c] / dx);
+      if (dz < 0.0) az = fmin(az, -Z[c] / dz);
+    }
+    ax = wmin(ax);
+    az = wmin(az);
+    const double bP = fmin(1.0, P.eta * ax);
+    const double bD = fmin(1.0, P.eta * az);
+    if (g_trace) {
+      if (lane == 0) {
+        int slot = atomicAdd(&g_trace_n, 1);
+        if (slot < g_trace_cap)
+          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, pr.relres, pr.rec_relres, dmn, dmx, mu, rbn, rcn, gap, bP, bD};
+      }
+    }
+    bool bad = false;
+#pragma unroll 4
+    for (int c = lane; c < Q; c += 32) {
+      if (c >= n && !(SC[c - n] & PRESENT)) continue;
+      double xn = X[c] + bP * V[c];
+      double zn = Z[c] + bD * D2[c];
+      X[c] = xn;
+      Z[c] = zn;
+      bad |= !isfinite(xn) || !isfinite(zn);
+    }
+    for (int j = lane; j < m; j += 32) {
+      if (!(SC[j] & PRESENT)) continue;
+      double yn = Y[j] + bD * DY[j];
+      Y[j] = yn;
+      bad |= !isfinite(yn);
+    }
+    __syncwarp();
+    ++it;
+    if (__any_sync(FULL, bad)) {
+      out.status |= ST_NUMERIC;
+      break;
+    }
+  }
+  ALP_TICK(F, CY_IPM, tk);
+  out.iters = it;
+  return out;
+}
+
+
+// MALP-A / MALP-B decode of one frame (Alg. 3; outputs P:143, C-11..C-15).
+__device__ void decode_frame(Frame& F, const Params& P, const double* g, long long f,
+                             const DecodeOut& O) {
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
+  const int n = C.n, m = C.m, lane = F.lane;
+  double cm = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    double gi = g[i];
+    uint8_t fl = gi < 0.0;  // eq.`initial constraints` P:147-155: u^0 = hard decision
+    F.flip[i] = fl;
+    F.u[i] = fl ? 1.0 : 0.0;
+    cm = fmax(cm, fabs(gi));
+  }
+  for (int j = lane; j < m; j += 32) {
+    F.mask[j] = 0;
+    F.y[j] = 0.0;
+  }
+  const double cmax = wmax(cm);
+  __syncwarp();
+  int status = 0, lp_solves = 0, ipm_iters = 0, pcg_iters = 0, max_p = 0;
+  int solves = 0, p4_fail = 0, true_fail = 0;
+  double max_rec = 0.0, max_true = 0.0;
+  bool last_lp_bad = false;   // the last solved LP did not converge (IPM cap / non-finite)
+  double pcg_bytes = 0.0;
+  if (lane < 8) F.cyc[lane] = 0;
+  __syncwarp();
+  long long tk = clock64();
+  for (int k = 0;; ++k) {
+    bool changed = cut_search(F, P);
+    if (!changed) break;
+    if (k == P.alp_max_iter) {
+      status |= ST_ALP_MAXITER;
+      break;
+    }
+    // Reading C-12: the LP (hence u^k and the next cut search) is a function of the pool, so
+    // a pool equal to that of an LP already solved repeats forever: stop with the last solved
+    // u (G2) and the cap status.  Pools are compared by a 64-bit order-independent hash.
+    {
+      unsigned long long hsh = 0ull;
+      for (int j = lane; j < m; j += 32) {
+        unsigned long long v = ((unsigned long long)(unsigned)j << 16) | F.mask[j];
+        v *= 0x9E3779B97F4A7C15ull;
+        v ^= v >> 29;
+        v *= 0xBF58476D1CE4E5B9ull;
+        v ^= v >> 32;
+        hsh += (F.mask[j] & PRESENT) ? v : 0ull;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) hsh += __shfl_xor_sync(FULL, hsh, o);
+      bool seen = false;
+      for (int t = lane; t < k; t += 32) seen |= (F.hist[t] == hsh);
+      if (__any_sync(FULL, seen)) {
+        status |= ST_ALP_MAXITER;
+        break;
+      }
+      if (lane == 0) F.hist[k] = hsh;
+      __syncwarp();
+    }
+    int p, nact;
+    double bmax;
+    build_signs(F, true, p, nact, bmax);
+    ALP_TICK(F, CY_CUT, tk);
+    ++lp_solves;
+    max_p = max(max_p, p);
+    IpmOut o = ipm_solve(F, P, g, p, nact, bmax, cmax, f, lp_solves);
+    status |= o.status;
+    last_lp_bad = (o.status & (ST_IPM_MAXITER | ST_NUMERIC)) != 0;
+    ipm_iters += o.iters;
+    pcg_iters += o.pcg_iters;
+    pcg_bytes += o.pcg_bytes;
+    solves += o.solves;
+    p4_fail += o.p4_fail;
+    true_fail += o.true_fail;
+    max_rec = fmax(max_rec, o.max_rec);
+    max_true = fmax(max_true, o.max_true);
+    for (int i = lane; i < n; i += 32) {
+      double xi = F.x[i];
+      F.u[i] = F.flip[i] ? 1.0 - xi : xi;
+    }
+    __syncwarp();
+    tk = clock64();
+    // Reading C-30: an LP whose IPM ended on a non-finite iterate or at the Newton-step cap
+    // gives no trustworthy u for the next cut search, so the frame's decode stops there
+    // (status bits set, last u output; `stop_on_lp_failure = 0` keeps going).
+    if ((o.status & ST_NUMERIC) || (P.stop_on_lp_failure && (o.status & ST_IPM_MAXITER))) break;
+  }
+  ALP_TICK(F, CY_CUT, tk);
+  // outputs: hard decision, objective gamma^T u, g_max, ML certificate
+  double obj = 0.0, gm = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    double ui = F.u[i];
+    obj += g[i] * ui;
+    gm = fmax(gm, fmin(ui, 1.0 - ui));
+    O.hard[f * n + i] = (ui > 0.5) ? 1 : 0;
+    if (O.u_out) O.u_out[f * n + i] = ui;
+  }
+  bool parity_bad = false;
+  for (int j = lane; j < m; j += 32) {
+    int deg = C.chk_deg[j];
+    int par = 0;
+    for (int t = 0; t < deg; ++t) par ^= (F.u[chk_nb(C, j, t)] > 0.5) ? 1 : 0;
+    parity_bad |= (par != 0);
+    uint16_t mk = F.mask[j];
+    if (O.y_out) O.y_out[f * m + j] = (mk & PRESENT) ? F.y[j] : 0.0;
+    if (O.mask_out) O.mask_out[f * m + j] = mk;
+  }
+  obj = wsum(obj);
+  gm = wmax(gm);
+  bool pbad = __any_sync(FULL, parity_bad);
+  if (lane == 0) {
+    O.objective[f] = obj;
+    // ML certificate (C-11): an integral codeword that is the optimum of the LP; an LP
+    // whose IPM did not converge proves nothing, so its u never certifies (C-31)
+    O.cert[f] = (gm <= P.tau_cert && !pbad && !last_lp_bad) ? 1 : 0;
+    if (O.status) O.status[f] = status;
+    if (O.stats) {
+      alp_frame_stats st;
+      st.lp_solves = lp_solves;
+      st.ipm_iters = ipm_iters;
+      st.pcg_iters = pcg_iters;
+      st.max_p = max_p;
+      st.pcg_solves = solves;
+      st.pcg_p4_fail = p4_fail;
+      st.pcg_true_fail = true_fail;
+      st.reserved = 0;
+      st.max_rec_relres = max_rec;
+      st.max_true_relres = max_true;
+      st.g_max = gm;
+      st.pcg_bytes = pcg_bytes;
+      st.cyc_cut = F.cyc[CY_CUT];
+      st.cyc_ipm = F.cyc[CY_IPM];
+      st.cyc_build = F.cyc[CY_BUILD];
+      st.cyc_spmv = F.cyc[CY_SPMV];
+      st.cyc_sweep = F.cyc[CY_SWEEP];
+      st.cyc_pcg_other = F.cyc[CY_PCG];
+      st.cyc_sort = F.cyc[CY_SORT];
+      st.cyc_peel = F.cyc[CY_PEEL];
+      O.stats[f] = st;
+    }
+  }
+  __syncwarp();
+}
+
+#ifndef ALP_MINB
+#define ALP_MINB 1
+#endif
+__global__ void __launch_bounds__(128, ALP_MINB) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
+                                                        char* slots,
+                                                        const double* __restrict__ llr,
+                                                        long long n_frames, DecodeOut O,
+                                                        unsigned long long* counter) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ DCode sC;    // code / layout descriptors in shared memory: the Frame's pointers to
+  __shared__ Layout sL;   // them must not land in local memory
+  if (threadIdx.x == 0) sL = L;
+  DCode Cs;
+  stage_graph(C, G, smem, Cs);
+  if (threadIdx.x == 0) sC = Cs;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  Frame F;
+  char* slot = slots + gw * L.slot_bytes;
+  frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
+  __shared__ long long s_cyc[4][8];   // phase clocks in shared memory (a global RMW per tick
+  F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
+  while (true) {
+    long long f = 0;
+    if (lane == 0) f = (long long)atomicAdd(counter, 1ull);   // 64-bit: no wrap at any n_frames
+    f = __shfl_sync(FULL, f, 0);
+    if (f >= n_frames) break;
+    decode_frame(F, P, llr + f * C.n, f, O);
+  }
+}
+
+
+// Isolated step solve (eq.`Delta y` P:479) per system: signs, D^2, Alg. 7, PCG.
+__global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout L, GraphSmem G,
+                                                      char* slots, long long n_sys, StepIO io,
+                                                      unsigned long long* counter) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ DCode sC;
+  __shared__ Layout sL;
+  if (threadIdx.x == 0) sL = L;
+  DCode Cs;
+  stage_graph(C, G, smem, Cs);
+  if (threadIdx.x == 0) sC = Cs;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  Frame F;
+  char* slot = slots + gw * L.slot_bytes;
+  frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
+  const int n = C.n, m = C.m, Q = C.Q;
+  while (true) {
+    long long s = 0;
+    if (lane == 0) s = (long long)atomicAdd(counter, 1ull);
+    s = __shfl_sync(FULL, s, 0);
+    if (s >= n_sys) break;
+    for (int j = lane; j < m; j += 32) F.mask[j] = io.masks[s * m + j];
+    for (int i = lane; i < n; i += 32) F.flip[i] = io.flip ? (io.flip[s * n + i] ? 1 : 0) : 0;
+    __syncwarp();
+    int p, nact;
+    double bmax;
+    build_signs(F, false, p, nact, bmax);
+    for (int c = lane; c < Q; c += 32) {
+      double dd = io.d[s * Q + c];
+      F.d2[c] = dd * dd;
+    }
+    for (int j = lane; j < m; j += 32) F.w[j] = (F.sgnC_()[j] & PRESENT) ? io.r[s * m + j] : 0.0;
+    __syncwarp();
+    int nLb = 0, nLf = 0;
+    const bool mtm = (P.precond == 0) && p > 0;
+    if (mtm) build_precond(F, p, nLb, nLf);
+    if ((io.prow || io.pcol)) {
+      if (mtm) write_pivots(F, p, io.prow ? io.prow + s * m : nullptr, io.pcol ? io.pcol + s * m : nullptr);
+      else
+        for (int k = lane; k < m; k += 32) {
+          if (io.prow) io.prow[s * m + k] = -1;
+          if (io.pcol) io.pcol[s * m + k] = -1;
+        }
+    }
+    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, P.pcg_rel_tol, true);
+    for (int j = lane; j < m; j += 32) io.dy[s * m + j] = (F.sgnC_()[j] & PRESENT) ? F.dy_()[j] : 0.0;
+    if (lane == 0) {
+      if (io.iters) io.iters[s] = pr.iters;
+      if (io.relres) io.relres[s] = pr.relres;
+      if (io.status) io.status[s] = pr.status;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace ALP_NS
+}  // namespace alp
+#undef ALP_SH
+#undef ALP_GL_SM
+#undef ALP_GL
+#undef ALP_SHA

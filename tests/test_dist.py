@@ -76,3 +76,21 @@ def test_gloo_world_size_2_reduction():
 def test_single_process_reduce_is_identity():
     c, t = reduce_run(np.array([1.0, 2.0]), 3.5)
     assert c.tolist() == [1.0, 2.0] and t == 3.5
+
+
+def test_bench_launches_its_own_ranks():
+    """`bench.py --gpus 2` without a torch.distributed environment launches 2 ranks itself
+    (torch.distributed.run on 127.0.0.1); exercised on CPU through the oracle reference arm,
+    where rank 0 alone prints the JSON line and reports n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--cpu-seconds", "2"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
