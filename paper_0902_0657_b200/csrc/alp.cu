@@ -71,7 +71,7 @@ struct StepIO {
 using namespace alp;
 
 struct alp_code {
-  int n, m, dc, dv, E;
+  int n, m, dc, dv, dcr, dvr, E;   // dc, dv: padded strides of chk_var / var_chk; dcr, dvr: degrees
   uint16_t* d_chk_var;
   uint8_t* d_chk_deg;
   uint16_t* d_var_chk;
@@ -100,9 +100,11 @@ DCode make_dcode(const alp_code* c) {
   C.m = c->m;
   C.dc = c->dc;
   C.dv = c->dv;
+  C.dcr = c->dcr;
+  C.dvr = c->dvr;
   C.Q = c->n + c->m;
   C.W = (C.Q + 63) / 64;
-  C.RB = (c->dc + 1 <= 8) ? 8 : 16;   // back-record u16 words: head + <= d_c - 1 deps
+  C.RB = (c->dcr + 1 <= 8) ? 8 : 16;   // back-record u16 words: head + <= d_c - 1 deps
   C.chk_var = c->d_chk_var;
   C.chk_deg = c->d_chk_deg;
   C.var_chk = c->d_var_chk;
@@ -215,7 +217,7 @@ bool make_layout_sm(const DCode& C, Layout& L) {
   L.s_cnt = s(Q);
   L.s_xr = s(2 * Q);
   L.s_bm = s(8 * (size_t)C.W);
-  L.RS = (C.dc + 1 <= 8) ? 8 : 16;
+  L.RS = (C.dcr + 1 <= 8) ? 8 : 16;
   L.s_rrank = s(2 * m * (size_t)L.RS);
   const size_t endE = std::max(a, endSort);
   L.smem_bytes = (int)al(std::max(endD, endE), 128);
@@ -244,7 +246,7 @@ Layout make_layout(const DCode& C, int smem_budget) {
   L.s_cnt = s(Q);
   L.s_xr = s(2 * Q);
   L.s_bm = s(8 * (size_t)C.W);
-  L.RS = (C.dc + 1 <= 8) ? 8 : 16;
+  L.RS = (C.dcr + 1 <= 8) ? 8 : 16;
   L.s_rrank = s(2 * (size_t)m * L.RS);
   L.s_pos = s(2 * m);
   L.s_pcol = s(2 * m);
@@ -560,6 +562,11 @@ alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const i
   if ((long long)n + m > 65535) return fail(ALP_ERR_UNSUPPORTED, "n + m > 65535");
   if (m > 32767) return fail(ALP_ERR_UNSUPPORTED, "m > 32767 (15-bit row ids in the sweep records)");
   if (dv == 0) dv = 1;
+  // padded strides (vector loads of a whole row / column list): checks 8 or 16 u16 per row,
+  // variables DVMAX = 4 u16; the real maximum degrees are kept beside them
+  const int dcr = dc, dvr = dv;
+  dc = (dcr <= 8) ? 8 : 16;
+  dv = DVMAX;
   std::vector<uint16_t> chk_var((size_t)m * dc, 0xffff), var_chk((size_t)n * dv, 0xffff);
   std::vector<uint8_t> chk_deg(m), var_slot((size_t)n * dv, 0), var_deg(n, 0);
   for (int j = 0; j < m; ++j) {
@@ -578,6 +585,8 @@ alp_status alp_code_create(int32_t n, int32_t m, const int32_t* row_ptr, const i
   c->m = m;
   c->dc = dc;
   c->dv = dv;
+  c->dcr = dcr;
+  c->dvr = dvr;
   c->E = E;
   cudaError_t e;
   auto up = [&](void** dst, const void* src, size_t bytes) -> bool {

@@ -18,6 +18,17 @@
 #ifndef ALP_HEAVY
 #define ALP_HEAVY
 #endif
+// Per-phase call boundaries (tuning experiments): a real call gives the phase its own register
+// allocation at the price of passing the Frame through memory.
+#ifndef ALP_CALL_PCG
+#define ALP_CALL_PCG ALP_HEAVY
+#endif
+#ifndef ALP_CALL_BUILD
+#define ALP_CALL_BUILD ALP_HEAVY
+#endif
+#ifndef ALP_CALL_IPM
+#define ALP_CALL_IPM ALP_HEAVY
+#endif
 
 #ifndef ALP_DEVICE_TYPES
 #define ALP_DEVICE_TYPES
@@ -47,6 +58,7 @@ struct Params {
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
 struct DCode {
   int n, m, dc, dv, Q, W, RB;             // Q = n + m columns, W = bitmap words, RB = back-record u16 (8/16)
+  int dcr, dvr;                           // maximum check / variable degree (dc, dv: padded strides 8|16, 4)
   const uint16_t* __restrict__ chk_var;   // [m][dc] sorted variables of each check, 0xffff padded
   const uint8_t* __restrict__ chk_deg;    // [m]
   const uint16_t* __restrict__ var_chk;   // [n][dv] checks of each variable, 0xffff padded
@@ -418,7 +430,7 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
 // chunks, passes whose digit is the same for every key skipped) orders them: descending float
 // weight, ascending column on equal floats.  Runs of equal float keys are then re-ordered by the exact fp64 weight (ties
 // -> lower column).  Result: order[r] = column of rank r (r < nv), returns nv.
-// Buffers (shared window, sort phase): kA/kB u32[Q], cA/cB u16[Q], offs u32[16][32]; order
+// Buffers (shared window, sort phase): kA/kB u32[Q], cA/cB u16[Q]; order
 // u16[Q] must not overlap them (layout: s_order, then s_sortk).
 // =====================================================================================
 __device__ ALP_HEAVY int sort_columns(const Frame& F) {
@@ -432,8 +444,8 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   uint32_t* kB = kA + C.Q;
   uint16_t* cA = reinterpret_cast<uint16_t*>(kB + C.Q);
   uint16_t* cB = cA + C.Q;
-  uint32_t* offs = reinterpret_cast<uint32_t*>(F.sm + L.s_sorth);   // [16 digits][32 lanes]
   uint16_t* order = F.S<uint16_t>(L.s_order);
+  uint32_t* offs = F.S<uint32_t>(L.s_sorth);   // [16 digits][32 lanes]
   const unsigned lt = (1u << F.lane) - 1u;
   int nv = 0;
   for (int c0 = 0; c0 < C.Q; c0 += 32) {
@@ -474,7 +486,8 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
       q2 += (w == 2) ? inc : 0ull;
       q3 += (w == 3) ? inc : 0ull;
     }
-    // exclusive offsets per (digit, lane); a pass whose digit is the same for every key is skipped
+    // exclusive offsets per (digit, lane) in a [16 digits][32 lanes] table (conflict-free);
+    // a pass whose digit is the same for every key is skipped
     int base = 0;
     bool skip = false;
 #pragma unroll
@@ -718,37 +731,41 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
 // Sweep dependencies of the pivot on row R (A_M is upper triangular in pick order):
 //  back  (A_M f = r):   the other pivot columns of row R -> their pivot rows (picked later)
 //  fwd   (A_M^T z = g): the other present rows of column C_k (killed earlier)
-// Encoded row | (coefficient < 0) << 31.
-__device__ __forceinline__ int back_deps(const Frame& F, int R, int* deps) {
+// Encoded row | (coefficient < 0) << 31, in FIXED slots (back: position t in N(R), forward:
+// position k in the column's check list) with DEP_NONE where there is none, so the arrays stay
+// in registers (no dynamically indexed local arrays).
+constexpr int DEP_NONE = 0x40000000;
+template <int DCT>
+__device__ __forceinline__ void back_deps(const Frame& F, int R, int (&deps)[DCT]) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const uint16_t* poc = F.S<uint16_t>(F.L->s_poc);
-  int deg = C.chk_deg[R];
-  uint16_t s = F.sgnC_()[R];
-  int pc = F.S<uint16_t>(F.L->s_pcol)[R];
-  int nd = 0;
-  for (int t = 0; t < deg; ++t) {
-    int c = chk_nb(C, R, t);
-    if (c == pc) continue;
-    uint16_t rr = poc[c];
-    if (rr != NONE16) deps[nd++] = (int)rr | (int)(((unsigned)(s >> t) & 1u) << 31);
-  }
-  return nd;
-}
-__device__ __forceinline__ int fwd_deps(const Frame& F, int R, int* deps) {
-  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
-  int c = F.S<uint16_t>(F.L->s_pcol)[R];
-  int nd = 0;
-  if (c < C.n) {
-    uint8_t s = F.sgnV_()[c];
-    int dv = C.var_deg[c];
-    for (int k = 0; k < dv; ++k) {
-      if (!((s >> k) & 1)) continue;
-      int j = var_ck(C, c, k);
-      if (j == R) continue;
-      deps[nd++] = j | (int)(((unsigned)(s >> (4 + k)) & 1u) << 31);
+  const int deg = C.chk_deg[R];
+  const uint16_t s = F.sgnC_()[R];
+  const int pc = F.S<uint16_t>(F.L->s_pcol)[R];
+#pragma unroll
+  for (int t = 0; t < DCT; ++t) {
+    int v = DEP_NONE;
+    if (t < deg) {
+      const int c = C.chk_var[R * C.dc + t];
+      const uint16_t rr = (c == pc) ? NONE16 : poc[c];
+      if (rr != NONE16) v = (int)rr | (int)(((unsigned)(s >> t) & 1u) << 31);
     }
+    deps[t] = v;
   }
-  return nd;
+}
+__device__ __forceinline__ void fwd_deps(const Frame& F, int R, int (&deps)[DVMAX]) {
+  const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
+  const int c = F.S<uint16_t>(F.L->s_pcol)[R];
+  const uint8_t s = (c < C.n) ? F.sgnV_()[c] : (uint8_t)0;
+#pragma unroll
+  for (int k = 0; k < DVMAX; ++k) {
+    int v = DEP_NONE;
+    if ((s >> k) & 1) {
+      const int j = C.var_chk[c * C.dv + k];
+      if (j != R) v = j | (int)(((unsigned)(s >> (4 + k)) & 1u) << 31);
+    }
+    deps[k] = v;
+  }
 }
 // sign of the diagonal entry A[R, C_k]
 __device__ __forceinline__ int diag_neg(const Frame& F, int R) {
@@ -766,40 +783,51 @@ __device__ __forceinline__ int diag_neg(const Frame& F, int R) {
 // Pivots are processed in chunks of 32 in dependency order (fwd: ascending k, back:
 // descending k); dependencies inside the chunk are resolved by shuffle fixed-point rounds.
 // lv is indexed by pivot k.  Returns the number of levels.
-template <bool FWD>
-__device__ int compute_levels(const Frame& F, int p, uint16_t* lv) {
+template <bool FWD, int ND>
+__device__ int compute_levels_t(const Frame& F, int p, uint16_t* lv) {
   const uint16_t* prow = F.S<uint16_t>(F.L->s_prow);
   const uint16_t* pos = F.S<uint16_t>(F.L->s_pos);
   int maxlv = 0;
   for (int c0 = 0; c0 < p; c0 += 32) {
-    int k = FWD ? (c0 + F.lane) : (p - 1 - c0 - F.lane);
-    bool valid = FWD ? (k < p) : (k >= 0);
-    int deps[DCMAX];
-    int nd = 0;
+    const int k = FWD ? (c0 + F.lane) : (p - 1 - c0 - F.lane);
+    const bool valid = FWD ? (k < p) : (k >= 0);
+    int deps[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) deps[d] = DEP_NONE;
     if (valid) {
-      int R = prow[k];
-      nd = FWD ? fwd_deps(F, R, deps) : back_deps(F, R, deps);
+      const int R = prow[k];
+      if constexpr (FWD) fwd_deps(F, R, deps);
+      else back_deps<ND>(F, R, deps);
     }
-    int ext = 0, nin = 0;
-    int inl[DCMAX];
-    for (int d = 0; d < nd; ++d) {
-      int kd = pos[deps[d] & 0x7fffffff];
-      int off = FWD ? (kd - c0) : (p - 1 - c0 - kd);
-      if (off >= 0 && off < 32) inl[nin++] = off;
-      else ext = max(ext, (int)lv[kd] + 1);
-    }
-    int ninmax = wmaxi(nin);
-    int cur = ext;
-    for (int it = 0; it <= 32; ++it) {
-      int nw = ext;
-      for (int d = 0; d < ninmax; ++d) {
-        int src = (d < nin) ? inl[d] : F.lane;
-        int vv = __shfl_sync(FULL, cur, src);
-        if (d < nin) nw = max(nw, vv + 1);
+    int ext = 0, anyin = 0;
+    int inl[ND];   // in-chunk source lane of slot d, -1 if none
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      inl[d] = -1;
+      if (deps[d] != DEP_NONE) {
+        const int kd = pos[deps[d] & 0x7fff];
+        const int off = FWD ? (kd - c0) : (p - 1 - c0 - kd);
+        if (off >= 0 && off < 32) {
+          inl[d] = off;
+          anyin = 1;
+        } else {
+          ext = max(ext, (int)lv[kd] + 1);
+        }
       }
-      bool ch = (nw != cur);
-      cur = nw;
-      if (!__any_sync(FULL, ch)) break;
+    }
+    int cur = ext;
+    if (__any_sync(FULL, anyin)) {
+      for (int it = 0; it <= 32; ++it) {
+        int nw = ext;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const int vv = __shfl_sync(FULL, cur, inl[d] < 0 ? F.lane : inl[d]);
+          if (inl[d] >= 0) nw = max(nw, vv + 1);
+        }
+        const bool ch = (nw != cur);
+        cur = nw;
+        if (!__any_sync(FULL, ch)) break;
+      }
     }
     if (valid) {
       lv[k] = (uint16_t)cur;
@@ -808,6 +836,12 @@ __device__ int compute_levels(const Frame& F, int p, uint16_t* lv) {
     __syncwarp();
   }
   return wmaxi(maxlv) + 1;
+}
+
+template <bool FWD>
+__device__ int compute_levels(const Frame& F, int p, uint16_t* lv) {
+  if constexpr (FWD) return compute_levels_t<true, DVMAX>(F, p, lv);
+  else return (F.C->dcr <= 8) ? compute_levels_t<false, 8>(F, p, lv) : compute_levels_t<false, 16>(F, p, lv);
 }
 
 // Deterministic counting sort of pivots by level: lv[k] (level) is replaced by the slot of
@@ -855,7 +889,7 @@ __device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* of
 // Builds both sweep programs.  Record layout (ints):
 //  back  recB[slot*RB]: head = R | nd << 24 | diag_neg << 31, then nd deps (row | neg << 31)
 //  fwd   recF[slot*RF]: same head/deps; dinvF[slot] = 1 / d^2 of the pivot column
-__device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
+__device__ ALP_CALL_BUILD void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   long long t0 = clock64();
@@ -890,17 +924,32 @@ __device__ ALP_HEAVY void build_precond(const Frame& F, int p, int& nLb, int& nL
   // forward: RF = 4 words per pivot (d_v <= 4) + dinvF = 1 / d^2 of the pivot column.
   for (int k = F.lane; k < p; k += 32) {
     const int R = prow[k];
-    int deps[DCMAX];
     const int dn = diag_neg(F, R);
-    int nd = back_deps(F, R, deps);
     uint16_t* rb = F.recB_() + (size_t)lvB[k] * C.RB;
     rb[0] = (uint16_t)(R | (dn << 15));
-    for (int d = 1; d < C.RB; ++d) rb[d] = (d <= nd) ? (uint16_t)((deps[d - 1] & 0x7fff) | ((deps[d - 1] < 0) << 15)) : NODEP;
-    nd = fwd_deps(F, R, deps);
+    if (C.RB == 8) {
+      int deps[8];
+      back_deps<8>(F, R, deps);
+#pragma unroll
+      for (int t = 0; t < 7; ++t)
+        rb[1 + t] = (deps[t] == DEP_NONE) ? NODEP : (uint16_t)((deps[t] & 0x7fff) | ((deps[t] < 0) << 15));
+    } else {
+      int deps[16];
+      back_deps<16>(F, R, deps);
+#pragma unroll
+      for (int t = 0; t < 15; ++t)
+        rb[1 + t] = (deps[t] == DEP_NONE) ? NODEP : (uint16_t)((deps[t] & 0x7fff) | ((deps[t] < 0) << 15));
+    }
+    int fd[DVMAX];
+    fwd_deps(F, R, fd);
     const int sf = lvF[k];
     uint16_t* rf = F.recF_() + (size_t)sf * RF;
     rf[0] = (uint16_t)(R | (dn << 15));
-    for (int d = 1; d < RF; ++d) rf[d] = (d <= nd) ? (uint16_t)((deps[d - 1] & 0x7fff) | ((deps[d - 1] < 0) << 15)) : NODEP;
+    int at = 1;   // compact the <= d_v - 1 forward deps into RF - 1 slots (record in memory)
+#pragma unroll
+    for (int q = 0; q < DVMAX; ++q)
+      if (fd[q] != DEP_NONE && at < RF) rf[at++] = (uint16_t)((fd[q] & 0x7fff) | ((fd[q] < 0) << 15));
+    for (int q = at; q < RF; ++q) rf[q] = NODEP;
     F.dinvF_()[sf] = 1.0 / F.d2[pcol[R]];
   }
   __syncwarp();
@@ -1137,8 +1186,18 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, co
       const int deg = ok ? (int)chk_deg[j] : 0;
       hj[u] = ok ? hS[j] : 0.0;
       d2s[u] = ok ? d2s_[j] : 0.0;
+#ifdef ALP_SPMV_SCALAR
 #pragma unroll
       for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)chk_var[j * dc + t] : -1;
+#else
+      const uint4* rowq = reinterpret_cast<const uint4*>(chk_var + (size_t)(ok ? j : 0) * dc);
+      uint4 q4[(DCT + 7) / 8];
+#pragma unroll
+      for (int w = 0; w < (DCT + 7) / 8; ++w) q4[w] = rowq[w];
+      const uint16_t* qv = reinterpret_cast<const uint16_t*>(&q4[0]);
+#pragma unroll
+      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)qv[t] : -1;
+#endif
     }
     double acc[2];
 #pragma unroll
@@ -1174,8 +1233,8 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
   const uint16_t* __restrict__ var_chk = C.var_chk;
   const double* __restrict__ d2 = F.d2;
   ALP_GL_SM(d2);
-  const int n = C.n, dvm = C.dv;
-  const int dcs = C.dc;
+  const int n = C.n;
+  const int dcs = C.dcr;
   double hl = 0.0;
   // variable pass, U variables per lane per step: all their index / sign / weight loads are
   // issued before any gather, and all gathers before any store (the shared-memory store of
@@ -1191,9 +1250,15 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
       const bool ok = i < n;
       sv[u] = ok ? sgnV[i] : (uint8_t)0;
       dv[u] = ok ? d2[i] : 0.0;
+#ifdef ALP_SPMV_SCALAR
 #pragma unroll
-      for (int k = 0; k < DVMAX; ++k)
-        jn[u][k] = (ok && k < dvm && ((sv[u] >> k) & 1)) ? (int)var_chk[i * dvm + k] : -1;
+      for (int k = 0; k < DVMAX; ++k) jn[u][k] = ((sv[u] >> k) & 1) ? (int)var_chk[i * DVMAX + k] : -1;
+#else
+      const uint2 vq = ok ? reinterpret_cast<const uint2*>(var_chk)[i] : make_uint2(0xffffffffu, 0xffffffffu);
+      const int vv[DVMAX] = {(int)(vq.x & 0xffffu), (int)(vq.x >> 16), (int)(vq.y & 0xffffu), (int)(vq.y >> 16)};
+#pragma unroll
+      for (int k = 0; k < DVMAX; ++k) jn[u][k] = ((sv[u] >> k) & 1) ? vv[k] : -1;
+#endif
     }
     double acc[U];
 #pragma unroll
@@ -1300,7 +1365,7 @@ __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
 // stops with ST_PCG_FLOOR (attainable accuracy, informational).
 // Status: 0 = the last recursion met pcg_rel_tol (P4), ST_PCG_MAXITER (cap or stall),
 // ST_PCG_BREAKDOWN, ST_PCG_FLOOR (refine mode).  w is read from F.w; dy accumulates in F.dy_().
-__device__ ALP_HEAVY PcgResult pcg_solve(const Frame& F, const Params& P, int mode, int nLb, int nLf,
+__device__ ALP_CALL_PCG PcgResult pcg_solve(const Frame& F, const Params& P, int mode, int nLb, int nLf,
                                          double itol_rel, bool refine) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;

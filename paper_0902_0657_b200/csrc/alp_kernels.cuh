@@ -3,10 +3,89 @@
 namespace alp {
 namespace ALP_NS {
 
+constexpr int UB = 4;   // IPM-body elements per lane per step (load batching)
+
 struct IpmOut {
   int iters, status, pcg_iters, solves, p4_fail, true_fail;
   double pcg_bytes, max_rec, max_true;
 };
+
+// IPM-body row loops, specialised on the maximum check degree (DCT): UBR rows per lane per
+// step, every load of a step issued before any use (see ipm_solve).
+template <int DCT>
+__device__ __forceinline__ void ipm_rows_residual(const DCode& C, int lane, const uint16_t* __restrict__ SC,
+                                                  const double* __restrict__ B, const double* __restrict__ X,
+                                                  const double* __restrict__ Y, const double* __restrict__ Z,
+                                                  double* __restrict__ V, double* W, double* __restrict__ RBv,
+                                                  double* __restrict__ RCv, double& rbn, double& rcn, double& gap) {
+  constexpr int UBR = (DCT <= 6) ? UB : 1;
+  const int n = C.n, m = C.m;
+  for (int j0 = lane; j0 < m; j0 += 32 * UBR) {
+    double xs[UBR][DCT], bj[UBR], xsl[UBR], yj[UBR], zsl[UBR];
+    uint16_t sc[UBR];
+    int deg[UBR];
+#pragma unroll
+    for (int u = 0; u < UBR; ++u) {
+      const int j = min(j0 + 32 * u, m - 1);
+      sc[u] = (j0 + 32 * u < m) ? SC[j] : (uint16_t)0;
+      deg[u] = C.chk_deg[j];
+      bj[u] = B[j];
+      xsl[u] = X[n + j];
+      yj[u] = Y[j];
+      zsl[u] = Z[n + j];
+#pragma unroll
+      for (int t = 0; t < DCT; ++t) xs[u][t] = (t < deg[u]) ? X[C.chk_var[j * C.dc + t]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UBR; ++u) {
+      if (!(sc[u] & PRESENT)) continue;
+      const int j = j0 + 32 * u;
+      double acc = bj[u] - xsl[u];
+#pragma unroll
+      for (int t = 0; t < DCT; ++t)
+        if (t < deg[u]) acc = ((sc[u] >> t) & 1) ? acc + xs[u][t] : acc - xs[u][t];
+      W[j] = acc;
+      RBv[j] = acc;
+      rbn = fmax(rbn, fabs(acc));
+      const double rc = -yj[u] - zsl[u];
+      V[n + j] = rc;
+      RCv[n + j] = rc;
+      rcn = fmax(rcn, fabs(rc));
+      gap += xsl[u] * zsl[u];
+    }
+  }
+}
+
+template <int DCT>
+__device__ __forceinline__ void ipm_rows_w(const DCode& C, int lane, const uint16_t* __restrict__ SC, double* W,
+                                           const double* __restrict__ V) {
+  constexpr int UBR = (DCT <= 6) ? UB : 1;
+  const int n = C.n, m = C.m;
+  for (int j0 = lane; j0 < m; j0 += 32 * UBR) {
+    double vs[UBR][DCT], wj[UBR], vsl[UBR];
+    uint16_t sc[UBR];
+    int deg[UBR];
+#pragma unroll
+    for (int u = 0; u < UBR; ++u) {
+      const int j = min(j0 + 32 * u, m - 1);
+      sc[u] = (j0 + 32 * u < m) ? SC[j] : (uint16_t)0;
+      deg[u] = C.chk_deg[j];
+      wj[u] = W[j];
+      vsl[u] = V[n + j];
+#pragma unroll
+      for (int t = 0; t < DCT; ++t) vs[u][t] = (t < deg[u]) ? V[C.chk_var[j * C.dc + t]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UBR; ++u) {
+      if (!(sc[u] & PRESENT)) continue;
+      double acc = wj[u] + vsl[u];
+#pragma unroll
+      for (int t = 0; t < DCT; ++t)
+        if (t < deg[u]) acc = ((sc[u] >> t) & 1) ? acc - vs[u][t] : acc + vs[u][t];
+      W[j0 + 32 * u] = acc;
+    }
+  }
+}
 
 // =====================================================================================
 // Infeasible primal-dual path-following IPM (§IV-B) on the current pool LP
@@ -19,7 +98,7 @@ struct IpmOut {
 // Arrays: v holds r_c then D^2 r_c - Z^-1 r_e then dx; d2 holds D^2 then dz; w holds r_b
 // then the PCG right-hand side.
 // =====================================================================================
-__device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
+__device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const double* g, int p, int nact,
                             double bmax, double cmax, long long frame_id, int lp_id) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const int n = C.n, m = C.m, Q = C.Q, lane = F.lane;
@@ -63,42 +142,39 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
   int it = 0;
   while (true) {
     double rbn = 0.0, rcn = 0.0, gap = 0.0, cx = 0.0;
-#pragma unroll 4
-    for (int j = lane; j < m; j += 32) {
-      uint16_t s = SC[j];
-      if (!(s & PRESENT)) continue;
-      int deg = C.chk_deg[j];
-      double acc = B[j] - X[n + j];
-      for (int t = 0; t < deg; ++t) {
-        double xi = X[chk_nb(C, j, t)];
-        acc = ((s >> t) & 1) ? acc + xi : acc - xi;
+    // Every body loop below takes UB elements per lane per step and issues all of their loads
+    // (unconditionally: slot arrays cover every index, absent rows hold 0) before any use, so
+    // the L1/L2 round trips of a step overlap; presence only predicates the stores.
+    if (C.dcr <= 6) ipm_rows_residual<6>(C, lane, SC, B, X, Y, Z, V, W, RBv, RCv, rbn, rcn, gap);
+    else ipm_rows_residual<DCMAX>(C, lane, SC, B, X, Y, Z, V, W, RBv, RCv, rbn, rcn, gap);
+    for (int i0 = lane; i0 < n; i0 += 32 * UB) {
+      double gi[UB], zi[UB], xi[UB], ys[UB][DVMAX];
+      uint8_t sv[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int i = min(i0 + 32 * u, n - 1);
+        sv[u] = (i0 + 32 * u < n) ? SV[i] : (uint8_t)0;
+        gi[u] = g[i];
+        zi[u] = Z[i];
+        xi[u] = X[i];
+#pragma unroll
+        for (int k = 0; k < DVMAX; ++k) ys[u][k] = Y[min((int)C.var_chk[i * C.dv + k], m - 1)];
       }
-      W[j] = acc;
-      RBv[j] = acc;
-      rbn = fmax(rbn, fabs(acc));
-      double rc = -Y[j] - Z[n + j];
-      V[n + j] = rc;
-      RCv[n + j] = rc;
-      rcn = fmax(rcn, fabs(rc));
-      gap += X[n + j] * Z[n + j];
-    }
-#pragma unroll 4
-    for (int i = lane; i < n; i += 32) {
-      double ci = fabs(g[i]);
-      uint8_t s = SV[i];
-      int dv = C.var_deg[i];
-      double acc = ci - Z[i];
-      for (int k = 0; k < dv; ++k) {
-        if (!((s >> k) & 1)) continue;
-        double yj = Y[var_ck(C, i, k)];
-        acc = ((s >> (4 + k)) & 1) ? acc + yj : acc - yj;
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (i0 + 32 * u >= n) continue;
+        const int i = i0 + 32 * u;
+        const double ci = fabs(gi[u]);
+        double acc = ci - zi[u];
+#pragma unroll
+        for (int k = 0; k < DVMAX; ++k)
+          if ((sv[u] >> k) & 1) acc = ((sv[u] >> (4 + k)) & 1) ? acc + ys[u][k] : acc - ys[u][k];
+        V[i] = acc;
+        RCv[i] = acc;
+        rcn = fmax(rcn, fabs(acc));
+        gap += xi[u] * zi[u];
+        cx += ci * xi[u];
       }
-      V[i] = acc;
-      RCv[i] = acc;
-      rcn = fmax(rcn, fabs(acc));
-      double xi = X[i];
-      gap += xi * Z[i];
-      cx += ci * xi;
     }
     __syncwarp();
     rbn = wmax(rbn);
@@ -113,29 +189,31 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
       break;
     }
     const double mu = P.sigma * gap / q;
-#pragma unroll 4
-    for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(SC[c - n] & PRESENT)) continue;
-      double xc = X[c], zc = Z[c];
-      const double iz = 1.0 / zc;   // one division for D^2 = X Z^-1 and Z^-1 r_e
-      double d2 = xc * iz;
-      double re = mu - xc * zc;
-      D2[c] = d2;
-      V[c] = d2 * V[c] - re * iz;
+    for (int c0 = lane; c0 < Q; c0 += 32 * UB) {
+      double xc[UB], zc[UB], vc[UB];
+      bool ok[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int c = min(c0 + 32 * u, Q - 1);
+        ok[u] = (c0 + 32 * u < Q) && ((c < n) || (SC[c - n] & PRESENT));
+        xc[u] = X[c];
+        zc[u] = Z[c];
+        vc[u] = V[c];
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (!ok[u]) continue;
+        const int c = c0 + 32 * u;
+        const double iz = 1.0 / zc[u];   // one division for D^2 = X Z^-1 and Z^-1 r_e
+        const double d2 = xc[u] * iz;
+        const double re = mu - xc[u] * zc[u];
+        D2[c] = d2;
+        V[c] = d2 * vc[u] - re * iz;
+      }
     }
     __syncwarp();
-#pragma unroll 4
-    for (int j = lane; j < m; j += 32) {
-      uint16_t s = SC[j];
-      if (!(s & PRESENT)) continue;
-      int deg = C.chk_deg[j];
-      double acc = W[j] + V[n + j];
-      for (int t = 0; t < deg; ++t) {
-        double vi = V[chk_nb(C, j, t)];
-        acc = ((s >> t) & 1) ? acc - vi : acc + vi;
-      }
-      W[j] = acc;
-    }
+    if (C.dcr <= 6) ipm_rows_w<6>(C, lane, SC, W, V);
+    else ipm_rows_w<DCMAX>(C, lane, SC, W, V);
     __syncwarp();
     int nLb = 0, nLf = 0;
     const bool mtm = (P.precond == 0);
@@ -177,26 +255,50 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     // the primal row off by the step residual rho = r_b - A dx = w - Q dy.  That residual is
     // moved onto the preconditioner's basis columns: A_M f = rho (the back sweep of P:585),
     // dx_M += f, so A dx = r_b holds to rounding (reading C-32; R-1).
-#pragma unroll 4
-    for (int i = lane; i < n; i += 32) {
-      uint8_t s = SV[i];
-      int dv = C.var_deg[i];
-      double atdy = 0.0;
-      for (int k = 0; k < dv; ++k) {
-        if (!((s >> k) & 1)) continue;
-        double d = DY[var_ck(C, i, k)];
-        atdy = ((s >> (4 + k)) & 1) ? atdy - d : atdy + d;
+    for (int i0 = lane; i0 < n; i0 += 32 * UB) {
+      double d2i[UB], vi[UB], rci[UB], dys[UB][DVMAX];
+      uint8_t sv[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int i = min(i0 + 32 * u, n - 1);
+        sv[u] = (i0 + 32 * u < n) ? SV[i] : (uint8_t)0;
+        d2i[u] = D2[i];
+        vi[u] = V[i];
+        rci[u] = RCv[i];
+#pragma unroll
+        for (int k = 0; k < DVMAX; ++k) dys[u][k] = ((sv[u] >> k) & 1) ? DY[C.var_chk[i * C.dv + k]] : 0.0;
       }
-      const double dx = D2[i] * atdy - V[i];
-      V[i] = dx;
-      D2[i] = RCv[i] - atdy;   // dz
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (i0 + 32 * u >= n) continue;
+        const int i = i0 + 32 * u;
+        double atdy = 0.0;
+#pragma unroll
+        for (int k = 0; k < DVMAX; ++k)
+          if ((sv[u] >> k) & 1) atdy = ((sv[u] >> (4 + k)) & 1) ? atdy - dys[u][k] : atdy + dys[u][k];
+        V[i] = d2i[u] * atdy - vi[u];   // dx
+        D2[i] = rci[u] - atdy;          // dz
+      }
     }
-    for (int j = lane; j < m; j += 32) {
-      if (!(SC[j] & PRESENT)) continue;
-      const int c = n + j;
-      const double dx = D2[c] * DY[j] - V[c];
-      V[c] = dx;
-      D2[c] = RCv[c] - DY[j];
+    for (int j0 = lane; j0 < m; j0 += 32 * UB) {
+      double d2s[UB], dyj[UB], vs[UB], rcs[UB];
+      bool ok[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int j = min(j0 + 32 * u, m - 1);
+        ok[u] = (j0 + 32 * u < m) && (SC[j] & PRESENT);
+        d2s[u] = D2[n + j];
+        dyj[u] = DY[j];
+        vs[u] = V[n + j];
+        rcs[u] = RCv[n + j];
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (!ok[u]) continue;
+        const int c = n + j0 + 32 * u;
+        V[c] = d2s[u] * dyj[u] - vs[u];
+        D2[c] = rcs[u] - dyj[u];
+      }
     }
     __syncwarp();
     if (P.basis_correction && nLb > 0) {
@@ -227,12 +329,24 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
     }
     // ratio test (C-6)
     double ax = 1e308, az = 1e308;
-#pragma unroll 4
-    for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(SC[c - n] & PRESENT)) continue;
-      const double dx = V[c], dz = D2[c];
-      if (dx < 0.0) ax = fmin(ax, -X[c] / dx);
-      if (dz < 0.0) az = fmin(az, -Z[c] / dz);
+    for (int c0 = lane; c0 < Q; c0 += 32 * UB) {
+      double dxs[UB], dzs[UB], xc[UB], zc[UB];
+      bool ok[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int c = min(c0 + 32 * u, Q - 1);
+        ok[u] = (c0 + 32 * u < Q) && ((c < n) || (SC[c - n] & PRESENT));
+        dxs[u] = V[c];
+        dzs[u] = D2[c];
+        xc[u] = X[c];
+        zc[u] = Z[c];
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (!ok[u]) continue;
+        if (dxs[u] < 0.0) ax = fmin(ax, -xc[u] / dxs[u]);
+        if (dzs[u] < 0.0) az = fmin(az, -zc[u] / dzs[u]);
+      }
     }
     ax = wmin(ax);
     az = wmin(az);
@@ -246,14 +360,28 @@ __device__ ALP_HEAVY IpmOut ipm_solve(const Frame& F, const Params& P, const dou
       }
     }
     bool bad = false;
-#pragma unroll 4
-    for (int c = lane; c < Q; c += 32) {
-      if (c >= n && !(SC[c - n] & PRESENT)) continue;
-      double xn = X[c] + bP * V[c];
-      double zn = Z[c] + bD * D2[c];
-      X[c] = xn;
-      Z[c] = zn;
-      bad |= !isfinite(xn) || !isfinite(zn);
+    for (int c0 = lane; c0 < Q; c0 += 32 * UB) {
+      double dxs[UB], dzs[UB], xc[UB], zc[UB];
+      bool ok[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int c = min(c0 + 32 * u, Q - 1);
+        ok[u] = (c0 + 32 * u < Q) && ((c < n) || (SC[c - n] & PRESENT));
+        dxs[u] = V[c];
+        dzs[u] = D2[c];
+        xc[u] = X[c];
+        zc[u] = Z[c];
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (!ok[u]) continue;
+        const int c = c0 + 32 * u;
+        const double xn = xc[u] + bP * dxs[u];
+        const double zn = zc[u] + bD * dzs[u];
+        X[c] = xn;
+        Z[c] = zn;
+        bad |= !isfinite(xn) || !isfinite(zn);
+      }
     }
     for (int j = lane; j < m; j += 32) {
       if (!(SC[j] & PRESENT)) continue;

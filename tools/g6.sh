@@ -6,4 +6,4 @@ $CMD > gpurun_out/prof_plain_$TAG.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:alp_decode_kernel -s 1 -c 1 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "profile exit $?" >> gpurun_out/prof_plain_$TAG.log
-CFGS="4:8,4:11,4:6,2:8" F=16384 timeout 900 python tools/tune_smem.py > gpurun_out/tune6.log 2>&1
+
