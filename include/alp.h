@@ -111,7 +111,8 @@ typedef struct {
 
 typedef struct {
   int32_t variant;        /* 0 = MALP-A (Alg. 3), 1 = MALP-B                         */
-  int32_t precond;        /* 0 = column-wise greedy MTS (Alg. 7), 1 = none (plain CG)  */
+  int32_t precond;        /* 0 = column-wise greedy MTS (Alg. 7, default), 1 = none (plain CG,
+                             P:511), 2 = row-wise greedy MTS with diagonal expansion (Alg. 8) */
   double sigma;           /* centering: mu = sigma * x^T z / q (eq.`update mu`, C-5)   0.1    */
   double eta;             /* step damping of the ratio test (C-6)                0.99   */
   double gap_tol;         /* stop: x^T z <= gap_tol * (1 + |c^T x|) (C-8)               1e-9   */

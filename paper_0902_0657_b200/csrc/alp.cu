@@ -375,7 +375,8 @@ Params make_params(const alp_params* p) {
 alp_status check_params(const alp_params* p) {
   if (!p) return ALP_OK;
   if (p->variant < 0 || p->variant > 1) return fail(ALP_ERR_INVALID_ARG, "params.variant must be 0 or 1");
-  if (p->precond < 0 || p->precond > 1) return fail(ALP_ERR_INVALID_ARG, "params.precond must be 0 or 1");
+  if (p->precond < 0 || p->precond > 2)
+    return fail(ALP_ERR_INVALID_ARG, "params.precond must be 0 (Alg. 7), 1 (plain CG) or 2 (Alg. 8)");
   if (!(p->sigma > 0 && p->sigma < 1) || !(p->eta > 0 && p->eta < 1))
     return fail(ALP_ERR_INVALID_ARG, "params.sigma and params.eta must lie in (0,1)");
   if (p->alp_max_iter < 0 || p->alp_max_iter > 255 || p->ipm_max_iter < 0 || p->pcg_max_iter < 1)

@@ -728,6 +728,202 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
   else peel_picks_smem(F, p, order, rrank, RS, cntR, xrR, bm, pos, pcol, prow);
 }
 
+// =====================================================================================
+// Alg. 8, row-wise greedy search for the MTS, with diagonal expansion (line 14;
+// G11), SURVEY f-1.  Residual matrix state per row: live-column count and XOR of the live
+// column ids (the unique live column of a degree-1 row); a row bitmap of the degree-1 rows
+// not yet represented ("any degree-1 row" = the lowest index, as the oracle); the columns in
+// ascending weight order (ties -> lower index, C-10) for the erasures of line 11.  Every step
+// removes one column (picked on line 8 or erased on line 11), so the loop ends within q steps;
+// it stops as soon as no unrepresented row has a live column.  The pick sequence is lower
+// triangular; it is stored reversed, so that A_M is upper triangular in pivot order
+// like Alg. 7's and the level / sweep machinery is shared.  Returns the number of pivots (= p).
+// Arrays (peel window): asc = reversed `order` with runs of equal weight re-reversed;
+// rdeg (u8, bit 7 = represented) over `cnt`, rxor over `xr`, column-alive flags over `rank`,
+// row bitmap over `bm`; picks go to pcol / prow in reverse.
+template <int K>
+__device__ __noinline__ void peel_rowwise_t(const Frame& F, int p, int nv) {
+  const DCode C = *F.C;
+  const Layout& L = *F.L;
+  uint16_t* order = F.S<uint16_t>(L.s_order);
+  uint8_t* rdeg = F.S<uint8_t>(L.s_cnt);
+  uint16_t* rxor = F.S<uint16_t>(L.s_xr);
+  uint8_t* alive = reinterpret_cast<uint8_t*>(F.S<uint16_t>(L.s_rank));
+  unsigned long long* bm = F.S<unsigned long long>(L.s_bm);
+  uint16_t* pos = F.S<uint16_t>(L.s_pos);
+  uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
+  uint16_t* prow = F.S<uint16_t>(L.s_prow);
+  const uint16_t* sgnC = F.sgnC_();
+  const uint8_t* sgnV = F.sgnV_();
+  const double* d2 = F.d2;
+  const int m = C.m, n = C.n;
+  // ascending weight order: reverse `order`, then restore ascending column order inside runs of
+  // exactly equal weight (lane 0; only long at the first IPM step, where all weights are 1)
+  for (int r = F.lane; r < nv / 2; r += 32) {
+    const uint16_t a = order[r], b = order[nv - 1 - r];
+    order[r] = b;
+    order[nv - 1 - r] = a;
+  }
+  __syncwarp();
+  if (F.lane == 0) {
+    int r = 0;
+    while (r < nv) {
+      const double w = d2[order[r]];
+      int e = r + 1;
+      while (e < nv && d2[order[e]] == w) ++e;
+      for (int a = r, b = e - 1; a < b; ++a, --b) {
+        const uint16_t t = order[a];
+        order[a] = order[b];
+        order[b] = t;
+      }
+      r = e;
+    }
+  }
+  const int WR = (m + 63) >> 6;
+  for (int c = F.lane; c < C.Q; c += 32) alive[c] = 0;
+  for (int w = F.lane; w < WR; w += 32) bm[w] = 0ull;
+  __syncwarp();
+  for (int r = F.lane; r < nv; r += 32) alive[order[r]] = 1;
+  int live = 0;
+  for (int j = F.lane; j < m; j += 32) {
+    int dg = 0, x = 0;
+    if (sgnC[j] & PRESENT) {
+      const int deg = C.chk_deg[j];
+      for (int t = 0; t < deg; ++t) {
+        const int c = C.chk_var[j * C.dc + t];
+        ++dg;
+        x ^= c;
+      }
+      ++dg;          // the slack column n + j
+      x ^= n + j;
+      ++live;
+    }
+    rdeg[j] = (uint8_t)dg;
+    rxor[j] = (uint16_t)x;
+  }
+  live = wsumi(live);
+  __syncwarp();
+  unsigned long long wd[K];
+#pragma unroll
+  for (int kk = 0; kk < K; ++kk) wd[kk] = 0ull;   // no degree-1 row yet (every row has >= 2 columns)
+  int k = 0, e = 0;
+  while (live > 0) {
+    int j = -1;
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const unsigned bal = __ballot_sync(FULL, wd[kk] != 0ull);
+      if (bal && j < 0) {
+        const int src = __ffs(bal) - 1;
+        const unsigned long long w0 = __shfl_sync(FULL, wd[kk], src);
+        j = (32 * kk + src) * 64 + (__ffsll((long long)w0) - 1);
+      }
+    }
+    int c;
+    if (j >= 0) {                       // line 7-9: degree-1 row j, its unique live column
+      c = rxor[j];
+      if (F.lane == 0) {
+        prow[k] = (uint16_t)j;
+        pcol[k] = (uint16_t)c;
+        rdeg[j] = (uint8_t)(rdeg[j] | 0x80);   // represented
+      }
+      ++k;
+      --live;
+    } else {                            // line 11: erase the lowest-weight live column
+      while (true) {
+        const int r = e + F.lane;
+        const bool al = (r < nv) && alive[order[r]];
+        const unsigned bal = __ballot_sync(FULL, al);
+        if (bal) {
+          e += __ffs(bal) - 1;
+          break;
+        }
+        e += 32;
+      }
+      c = order[e];
+    }
+    if (F.lane == 0) alive[c] = 0;
+    __syncwarp();
+    // remove column c from A~: its rows lose one live column
+    int r = -1;
+    if (c < n) {
+      if (F.lane < DVMAX && ((sgnV[c] >> F.lane) & 1)) r = C.var_chk[c * C.dv + F.lane];
+    } else if (F.lane == 0) {
+      r = c - n;
+    }
+    int upd = -1, dead = 0;
+    if (r >= 0) {
+      const int dg = rdeg[r];
+      const int nd = (dg & 0x7f) - 1;
+      rdeg[r] = (uint8_t)((dg & 0x80) | nd);
+      rxor[r] = (uint16_t)(rxor[r] ^ c);
+      if (!(dg & 0x80) || r == j) {     // DEG1 holds only unrepresented rows (j just left it)
+        if (nd == 1 && !(dg & 0x80)) upd = (r << 1) | 1;
+        else if (nd == 0) {
+          upd = r << 1;
+          dead = (r != j) ? 1 : 0;      // an unrepresented row left without columns
+        }
+      }
+    }
+    live -= __popc(__ballot_sync(FULL, dead != 0));
+    int us[DVMAX];
+#pragma unroll
+    for (int t = 0; t < DVMAX; ++t) us[t] = __shfl_sync(FULL, upd, t);
+#pragma unroll
+    for (int t = 0; t < DVMAX; ++t) {
+      const int u = us[t];
+      if (u < 0) continue;
+      const int rr = u >> 1;
+      const int wi = rr >> 6;
+      if ((wi & 31) == F.lane) {
+        const unsigned long long bit = 1ull << (rr & 63);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+          if ((wi >> 5) == kk) wd[kk] = (u & 1) ? (wd[kk] | bit) : (wd[kk] & ~bit);
+      }
+    }
+    __syncwarp();
+  }
+  // diagonal expansion (line 14): every present row not represented gets its slack column
+  const unsigned lt = (1u << F.lane) - 1u;
+  for (int j0 = 0; j0 < m; j0 += 32) {
+    const int j = j0 + F.lane;
+    const bool need = (j < m) && (sgnC[j] & PRESENT) && !(rdeg[j] & 0x80);
+    const unsigned bal = __ballot_sync(FULL, need);
+    if (need) {
+      const int at = k + __popc(bal & lt);
+      prow[at] = (uint16_t)j;
+      pcol[at] = (uint16_t)(n + j);
+    }
+    k += __popc(bal);
+  }
+  __syncwarp();
+  // reverse into upper-triangular pivot order; pcol / pos become indexed by row (as Alg. 7's)
+  for (int t = F.lane; t < k / 2; t += 32) {
+    const uint16_t ra = prow[t], rb = prow[k - 1 - t];
+    const uint16_t ca = pcol[t], cb = pcol[k - 1 - t];
+    prow[t] = rb;
+    prow[k - 1 - t] = ra;
+    pcol[t] = cb;
+    pcol[k - 1 - t] = ca;
+  }
+  __syncwarp();
+  // pcol[] was filled in pick order; Alg. 7 keeps it indexed by row: convert through pos
+  for (int t = F.lane; t < k; t += 32) pos[prow[t]] = (uint16_t)t;
+  __syncwarp();
+  for (int t = F.lane; t < k; t += 32) rxor[prow[t]] = pcol[t];   // row -> column (rxor is dead)
+  __syncwarp();
+  for (int j = F.lane; j < m; j += 32) pcol[j] = rxor[j];
+  __syncwarp();
+  (void)p;
+}
+
+__device__ ALP_HEAVY void peel_rowwise(const Frame& F, int p, int nv) {
+  const int WR = (F.C->m + 63) >> 6;
+  if (WR <= 32) peel_rowwise_t<1>(F, p, nv);
+  else if (WR <= 128) peel_rowwise_t<4>(F, p, nv);
+  else peel_rowwise_t<16>(F, p, nv);
+}
+
 // Sweep dependencies of the pivot on row R (A_M is upper triangular in pick order):
 //  back  (A_M f = r):   the other pivot columns of row R -> their pivot rows (picked later)
 //  fwd   (A_M^T z = g): the other present rows of column C_k (killed earlier)
@@ -889,13 +1085,17 @@ __device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* of
 // Builds both sweep programs.  Record layout (ints):
 //  back  recB[slot*RB]: head = R | nd << 24 | diag_neg << 31, then nd deps (row | neg << 31)
 //  fwd   recF[slot*RF]: same head/deps; dinvF[slot] = 1 / d^2 of the pivot column
-__device__ ALP_CALL_BUILD void build_precond(const Frame& F, int p, int& nLb, int& nLf) {
+// Preconditioner build: the column ranking, then Alg. 7 (mts = 0, the default) or
+// Alg. 8 with diagonal expansion (mts = 2, SURVEY f-1), then the level schedules and the
+// sweep programs shared by both.
+__device__ ALP_CALL_BUILD void build_precond(const Frame& F, int p, int& nLb, int& nLf, int mts = 0) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   long long t0 = clock64();
-  sort_columns(F);
+  const int nv = sort_columns(F);
   long long t1 = clock64();
-  peel_columnwise(F, p);
+  if (mts == 2) peel_rowwise(F, p, nv);
+  else peel_columnwise(F, p);
   long long t2 = clock64();
   if (F.lane == 0) {
     F.cyc[CY_SORT] += t1 - t0;
@@ -1186,18 +1386,8 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, co
       const int deg = ok ? (int)chk_deg[j] : 0;
       hj[u] = ok ? hS[j] : 0.0;
       d2s[u] = ok ? d2s_[j] : 0.0;
-#ifdef ALP_SPMV_SCALAR
 #pragma unroll
       for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)chk_var[j * dc + t] : -1;
-#else
-      const uint4* rowq = reinterpret_cast<const uint4*>(chk_var + (size_t)(ok ? j : 0) * dc);
-      uint4 q4[(DCT + 7) / 8];
-#pragma unroll
-      for (int w = 0; w < (DCT + 7) / 8; ++w) q4[w] = rowq[w];
-      const uint16_t* qv = reinterpret_cast<const uint16_t*>(&q4[0]);
-#pragma unroll
-      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)qv[t] : -1;
-#endif
     }
     double acc[2];
 #pragma unroll
@@ -1250,15 +1440,9 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
       const bool ok = i < n;
       sv[u] = ok ? sgnV[i] : (uint8_t)0;
       dv[u] = ok ? d2[i] : 0.0;
-#ifdef ALP_SPMV_SCALAR
+      // scalar u16 index loads (measured: 16-byte vector loads of the padded rows were 1.8x slower)
 #pragma unroll
       for (int k = 0; k < DVMAX; ++k) jn[u][k] = ((sv[u] >> k) & 1) ? (int)var_chk[i * DVMAX + k] : -1;
-#else
-      const uint2 vq = ok ? reinterpret_cast<const uint2*>(var_chk)[i] : make_uint2(0xffffffffu, 0xffffffffu);
-      const int vv[DVMAX] = {(int)(vq.x & 0xffffu), (int)(vq.x >> 16), (int)(vq.y & 0xffffu), (int)(vq.y >> 16)};
-#pragma unroll
-      for (int k = 0; k < DVMAX; ++k) jn[u][k] = ((sv[u] >> k) & 1) ? vv[k] : -1;
-#endif
     }
     double acc[U];
 #pragma unroll

@@ -216,11 +216,11 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
     else ipm_rows_w<DCMAX>(C, lane, SC, W, V);
     __syncwarp();
     int nLb = 0, nLf = 0;
-    const bool mtm = (P.precond == 0);
+    const bool mtm = (P.precond == 0 || P.precond == 2);   // MTS-preconditioned PCG
     ALP_TICK(F, CY_IPM, tk);
     // the Alg. 7 triangular set is both the PCG preconditioner (precond = 0) and the basis of
     // the step's feasibility correction (C-32), so plain CG builds it too when that is on
-    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf);
+    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf, P.precond == 2 ? 2 : 0);
     ALP_TICK(F, CY_BUILD, tk);
     // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to well
     // below z ~ mu on the basic columns, so late in the IPM the recursion aims at
@@ -614,8 +614,8 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
     for (int j = lane; j < m; j += 32) F.w[j] = (F.sgnC_()[j] & PRESENT) ? io.r[s * m + j] : 0.0;
     __syncwarp();
     int nLb = 0, nLf = 0;
-    const bool mtm = (P.precond == 0) && p > 0;
-    if (mtm) build_precond(F, p, nLb, nLf);
+    const bool mtm = (P.precond == 0 || P.precond == 2) && p > 0;
+    if (mtm) build_precond(F, p, nLb, nLf, P.precond);
     if ((io.prow || io.pcol)) {
       if (mtm) write_pivots(F, p, io.prow ? io.prow + s * m : nullptr, io.pcol ? io.pcol + s * m : nullptr);
       else

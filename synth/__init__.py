@@ -12,9 +12,10 @@ from .codes import Code, regular_code, code_from_rows, CONFIG_CODES, config_code
 from .frames import (sigma2_for, awgn_frames, FrameBatch, CONFIGS, config_frames,
                      GF2Encoder)
 from .systems import StepSystems, c5_systems, odd_masks
+from .bsc import bsc_llr, bsc_frames
 
 __all__ = [
     "Code", "regular_code", "code_from_rows", "CONFIG_CODES", "config_code",
     "sigma2_for", "awgn_frames", "FrameBatch", "CONFIGS", "config_frames",
-    "GF2Encoder", "StepSystems", "c5_systems", "odd_masks",
+    "GF2Encoder", "StepSystems", "c5_systems", "odd_masks", "bsc_llr", "bsc_frames",
 ]

@@ -78,8 +78,9 @@ def code_from_dense(H: np.ndarray, name: str = "") -> Code:
                           H.shape[1], name)
 
 
-def regular_code(n: int, dv: int, dc: int, seed: int, name: str = "") -> Code:
-    """Seeded (dv, dc)-regular configuration-model code, double edges resampled."""
+def regular_code(n: int, dv: int, dc: int, seed: int, name: str = "", girth6: bool = False) -> Code:
+    """Seeded (dv, dc)-regular configuration-model code, double edges resampled; girth6 also
+    removes every 4-cycle (the paper's codes; reading C-21 keeps them for the configs)."""
     if (n * dv) % dc:
         raise ValueError("n*dv must be divisible by dc")
     E = n * dv
@@ -100,11 +101,44 @@ def regular_code(n: int, dv: int, dc: int, seed: int, name: str = "") -> Code:
         e = int(dups[0])
         e2 = int(rng.integers(E))
         pi[e], pi[e2] = pi[e2], pi[e]
+    if girth6:
+        # optional 4-cycle removal (C-21; the paper's codes): while two variables
+        # share two checks, swap the check socket of one edge of that cycle with a random edge
+        # (same stream), keeping the graph free of double edges
+        for _ in range(200 * E):
+            chk = pi // dc
+            cyc = _find_4cycle_edge(var_of_edge, chk, n, m, dv)
+            if cyc < 0:
+                break
+            e2 = int(rng.integers(E))
+            pi[cyc], pi[e2] = pi[e2], pi[cyc]
+            chk = pi // dc
+            key = var_of_edge.astype(np.int64) * m + chk
+            if np.unique(key).size != E:       # created a double edge: undo
+                pi[cyc], pi[e2] = pi[e2], pi[cyc]
+        else:
+            raise RuntimeError("4-cycle removal did not converge")
     chk = pi // dc
     rows: list[list[int]] = [[] for _ in range(m)]
     for e in range(E):
         rows[int(chk[e])].append(int(var_of_edge[e]))
-    return code_from_rows(rows, n, name or f"rnd({dv},{dc}) n={n} seed={seed}")
+    return code_from_rows(rows, n, name or f"rnd({dv},{dc}) n={n} seed={seed}" + (" girth6" if girth6 else ""))
+
+
+def _find_4cycle_edge(var_of_edge, chk, n, m, dv) -> int:
+    """An edge on some 4-cycle (two variables sharing two checks), or -1 if the graph has none."""
+    vc = chk.reshape(n, dv)
+    seen = {}
+    for i in range(n):
+        cs = sorted(int(c) for c in vc[i])
+        for a in range(dv):
+            for b in range(a + 1, dv):
+                key = (cs[a], cs[b])
+                if key in seen and seen[key] != i:
+                    # edge (i, cs[a]) lies on the cycle i - cs[a] - seen[key] - cs[b] - i
+                    return int(i * dv + list(vc[i]).index(cs[a]))
+                seen[key] = i
+    return -1
 
 
 # BASELINE.json configs (SURVEY.md §8(d) d.1 code seeds)

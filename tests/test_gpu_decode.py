@@ -298,3 +298,26 @@ def test_config4_golden_frames():
                 chol_fixes=int(o["chol_fixes"])) for o in gold]
     parity("C4_golden", code, fb.llr, g, orc)
     assert_certified(code, fb.llr, g)
+
+
+def test_config1_rowwise_mts_decode():
+    """SURVEY f-1: the decode with the row-wise MTS preconditioner (precond = 2, Alg. 8) reaches
+    the same LP outputs (P1-P3, P6) as the oracle."""
+    code = config_code(1)
+    fb = config_frames(1, frames=range(48))
+    g = gpu_decode(code, fb.llr, precond=2)
+    parity("C1_rowwise", code, fb.llr, g, oracle_decode(1, range(48)))
+    assert_certified(code, fb.llr, g)
+
+
+def test_bsc_jittered_frames_vs_oracle():
+    """SURVEY f-4: BSC frames with LLR jitter (synth/bsc.py) decode on the GPU to the
+    oracle's LP outputs (P1-P3) and certify (P6)."""
+    from synth import bsc_frames
+    code = config_code(1)
+    fb = bsc_frames(code, 0.04, 1e-3, 3003, range(48))
+    g = gpu_decode(code, fb.llr)
+    from oracle.lp import malp_decode
+    orc = [malp_decode(code, fb.llr[f]) for f in range(fb.F)]
+    parity("C1_bsc_jitter", code, fb.llr, g, orc)
+    assert_certified(code, fb.llr, g)

@@ -223,3 +223,82 @@ def test_c5_full_size_properties_and_sampled_parity():
     for k, s in enumerate(sample):
         _check_system(code, sy.masks[s], sy.d[s], sy.r[s], None, out, int(s), tol_dy=1e-8,
                       ref=orc[k][0], piv=(orc[k][1], orc[k][2]))
+
+
+def _check_rowwise(code, masks, d, r, flip=None, S=None):
+    """Alg. 8 on the GPU (precond = 2): the pivot sequence, read back in pick order, equals the
+    oracle's mts_rowwise (lowest-index degree-1 row, min-weight erasure, diagonal expansion)."""
+    from oracle.precond import mts_rowwise
+    out = _run(code, masks, d, r, flip, precond=2)
+    S = masks.shape[0] if S is None else S
+    for s in range(S):
+        A, rows = dense_step_matrix(code, masks[s], None if flip is None else flip[s])
+        if not rows:
+            continue
+        w2 = step_weights(code, d[s], rows)
+        col, row = mts_rowwise(A, w2)
+        p = len(rows)
+        exp_rows = [rows[rw] for rw in row][::-1]          # stored reversed (upper triangular)
+        exp_cols = [oracle_col_to_gpu(code, rows, c) for c in col][::-1]
+        assert list(out["prow"][s][:p]) == exp_rows, f"system {s}: row-wise pivot rows differ"
+        assert list(out["pcol"][s][:p]) == exp_cols, f"system {s}: row-wise pivot cols differ"
+        _check_system(code, masks[s], d[s], r[s], None if flip is None else flip[s], out, s, tol_dy=1e-8,
+                      check_pivots=False)
+    return out
+
+
+def test_rowwise_mts_matches_oracle_alg8():
+    """SURVEY f-1: Alg. 8 bit-exact vs the oracle on config-1 systems with partial
+    rows and flips, on all-equal weights (tie rules), and on config-5 systems."""
+    code = config_code(1)
+    S = 24
+    sy = c5_systems(range(S), code, lo=-3, hi=3, present_frac=0.7)
+    flip = np.random.default_rng(11).integers(0, 2, size=(S, code.n)).astype(np.uint8)
+    _check_rowwise(code, sy.masks, sy.d, sy.r, flip)
+    _check_rowwise(code, sy.masks, np.ones_like(sy.d), sy.r, flip)
+    code5 = config_code(5)
+    sy5 = c5_systems(range(8), code5, lo=-2, hi=2)
+    _check_rowwise(code5, sy5.masks, sy5.d, sy5.r)
+
+
+def test_thm5_rowwise_contains_basic_columns_near_integral_optimum():
+    """Thm 5: near the optimum of an LP with an integral solution, the row-wise MTS
+    contains every basic column.  Late-IPM weights are formed from the oracle's LP optimum x*
+    (basic: x* = 1 or slack > 0 -> d^2 = x*/(mu/x*), nonbasic -> d^2 = (mu/z)/z, z = 1), mu =
+    1e-8; the GPU's Alg. 8 pivot columns must include all basic columns.  Column-wise (Alg. 7,
+    for which the paper claims no such property) is reported for comparison."""
+    from oracle.lp import malp_decode, augmented_lp, ipm_solve
+    code = config_code(1)
+    fb = config_frames(1, frames=range(12))
+    cover_col = []
+    for f in range(fb.F):
+        o = malp_decode(code, fb.llr[f])
+        if o["cert"] != 1 or not o["pool"]:
+            continue
+        lp = augmented_lp(code, o["pool"], fb.llr[f])
+        x = ipm_solve(lp["A"], lp["b"], lp["c"])["x"]
+        basic = np.nonzero(x > 0.5)[0]                      # integral LP: x* in {0, 1} on std, slack >= 0
+        basic = np.array([c for c in range(lp["q"]) if x[c] > 1e-3])
+        mu = 1e-8
+        d2 = np.where(x > 1e-3, np.maximum(x, 1e-3) ** 2 / mu, mu)
+        rows = lp["rows"]
+        masks = np.zeros((1, code.m), dtype=np.uint16)
+        for rr, j in enumerate(rows):
+            masks[0, j] = o["masks"][j]
+        d = np.ones((1, code.n + code.m))
+        d[0, :code.n] = np.sqrt(d2[:code.n])
+        for rr, j in enumerate(rows):
+            d[0, code.n + j] = np.sqrt(d2[code.n + rr])
+        flip = (fb.llr[f:f + 1] < 0).astype(np.uint8)
+        r = np.random.default_rng(f).standard_normal((1, code.m))
+        outs = {}
+        for pc in (2, 0):
+            out = _run(code, masks, d, r, flip, precond=pc)
+            cols = set(int(c) for c in out["pcol"][0][:len(rows)])
+            gpu_basic = {c if c < code.n else code.n + rows[c - code.n] for c in basic}
+            outs[pc] = gpu_basic <= cols
+        assert outs[2], f"frame {f}: row-wise MTS misses a basic column (Thm 5)"
+        cover_col.append(outs[0])
+    assert cover_col, "no certified frame with cuts in the sample"
+    print(f"Thm 5: row-wise covers the basic set on {len(cover_col)}/{len(cover_col)} LPs; "
+          f"column-wise on {sum(cover_col)}/{len(cover_col)}")

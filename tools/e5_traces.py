@@ -5,10 +5,11 @@ IPM iterations 8 and 18 of a MALP-A LP, for an integral (1.5 dB) and a fractiona
 Here: our seeded n=2000 (3,6) code (4-cycles kept, reading C-21), the first frame at each SNR whose
 MALP-A decode has >= 3 LPs; the LP solved third is run by the ORACLE's IPM (direct Cholesky step)
 to capture the Newton systems at IPM iterations 8 and 18; each system is then solved on the GPU by
-ipm_step_pcg with the column-wise MTS preconditioner (precond=0, Alg. 7) and with plain CG
-(precond=1), capped at k = 1..K iterations, giving the TRUE relative residual ||w - Q dy||/||w||
-after k iterations (the paper plots the squared ratio, G15).  Output: gpurun_out/e5_traces.json.
-The incremental and row-wise MTS curves of the paper are not reproduced (Alg. 6/8 are oracle-only).
+ipm_step_pcg with the column-wise MTS preconditioner (precond=0, Alg. 7), the row-wise MTS with
+diagonal expansion (precond=2, Alg. 8) and plain CG (precond=1), capped at k = 1..K iterations,
+giving the TRUE relative residual ||w - Q dy||/||w|| after k iterations (the paper plots the
+squared ratio, G15).  Output: gpurun_out/e5_traces.json.  The incremental MTS curve (Alg. 6,
+O(q^2)) is not reproduced on the GPU (oracle only).
 """
 import json
 import os
@@ -71,7 +72,7 @@ for label, snr in (("integral_1.5dB", 1.5), ("fractional_1.0dB", 1.0)):
         td = torch.from_numpy(d).cuda()
         tr = torch.from_numpy(r).cuda()
         curves = {}
-        for name, pc in (("column-wise MTS", 0), ("CG", 1)):
+        for name, pc in (("column-wise MTS", 0), ("row-wise MTS", 2), ("CG", 1)):
             res = []
             for k in range(1, K + 1):
                 prm = alp.default_params(precond=pc, pcg_max_iter=k, pcg_rel_tol=1e-14)
