@@ -141,6 +141,10 @@ typedef struct {
   double pcg_forcing;     /* inexact-Newton forcing factor: inside the IPM the PCG recursion
                              aims at min(pcg_rel_tol, pcg_forcing * mu) (R-1); 0 =
                              plain pcg_rel_tol                                         1e-2   */
+  int32_t pcg_refine;     /* ipm_step_pcg only: 0 = the PCG recursion alone; 1 = fp64 iterative
+                             refinement from the true residual down to the fp64 evaluation floor
+                             (round 1); 2 = refinement with double-double residuals until the
+                             correction stops shrinking (C-27: forward error ~1e-13)     2      */
 } alp_params;
 
 /* Fills the defaults listed above (identical to the oracle's constants). */

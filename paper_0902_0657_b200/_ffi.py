@@ -17,7 +17,7 @@ class AlpParams(C.Structure):
         ("alp_max_iter", C.c_int32), ("ipm_max_iter", C.c_int32), ("pcg_max_iter", C.c_int32),
         ("warps_per_block", C.c_int32), ("smem_frames_per_sm", C.c_int32),
         ("stop_on_lp_failure", C.c_int32),
-        ("basis_correction", C.c_int32), ("pcg_forcing", C.c_double),
+        ("basis_correction", C.c_int32), ("pcg_forcing", C.c_double), ("pcg_refine", C.c_int32),
     ]
 
 

@@ -5,6 +5,7 @@
 // runs the whole adaptive-LP decode of that frame (Alg. 3 with the IPM of §IV-B and the
 // PCG of Alg. 4 preconditioned by Alg. 7) and writes its outputs; no host round trips.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <cstdio>
 #include <cstring>
@@ -159,7 +160,7 @@ size_t make_slot(const DCode& C, Layout& L) {
 //      bitmap, row ranks) overlay D.
 // d^2, w and the IPM arrays stay in the slot (L1/L2).  Returns false when the late arrays do
 // not fit P (then the generic mode is used).
-bool make_layout_sm(const DCode& C, Layout& L) {
+bool make_layout_sm(const DCode& C, Layout& L, bool sm_d2) {
   const size_t n = C.n, m = C.m, Q = C.Q;
   make_slot(C, L);
   L.win_global = 0;
@@ -196,6 +197,7 @@ bool make_layout_sm(const DCode& C, Layout& L) {
   };
   rel(RL_SGNC, 2 * m);
   rel(RL_SGNV, n);
+  if (sm_d2) rel(RL_D2, 8 * Q);   // d^2 too (fewer frames per SM; tuning)
   // D
   const size_t D0 = a;
   rel(RL_L, 8 * m);
@@ -328,7 +330,7 @@ GraphSmem make_graph_smem(const DCode& C) {
   G.o_chk_var = a(2 * (size_t)C.m * C.dc);
   G.o_chk_deg = a(C.m);
   G.o_var_chk = a(2 * (size_t)C.n * C.dv);
-  G.o_var_slot = a((size_t)C.n * C.dv);
+  G.o_var_slot = 0;   // not staged (build_signs reads it from global memory once per LP)
   G.o_var_deg = a(C.n);
   G.bytes = (int)al(o, 128);
   if (G.bytes > 48 * 1024) G = GraphSmem{0, 0, 0, 0, 0, 0};   // large codes: graph stays global
@@ -363,6 +365,7 @@ Params make_params(const alp_params* p) {
   P.stop_on_lp_failure = p->stop_on_lp_failure;
   P.basis_correction = p->basis_correction;
   P.pcg_forcing = p->pcg_forcing;
+  P.pcg_refine = p->pcg_refine;
   P.tau_viol = p->tau_viol;
   P.tau_act = p->tau_act;
   P.tau_cert = p->tau_cert;
@@ -381,6 +384,8 @@ alp_status check_params(const alp_params* p) {
     return fail(ALP_ERR_INVALID_ARG, "params.sigma and params.eta must lie in (0,1)");
   if (p->alp_max_iter < 0 || p->alp_max_iter > 255 || p->ipm_max_iter < 0 || p->pcg_max_iter < 1)
     return fail(ALP_ERR_INVALID_ARG, "iteration caps: 0 <= alp_max_iter <= 255, ipm >= 0, pcg >= 1");
+  if (p->pcg_refine < 0 || p->pcg_refine > 2)
+    return fail(ALP_ERR_INVALID_ARG, "params.pcg_refine must be 0, 1 or 2");
   if (p->warps_per_block < 0 || p->warps_per_block > 4 || p->smem_frames_per_sm < 0 || p->smem_frames_per_sm > 32)
     return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..4, smem_frames_per_sm 0..32");
   return ALP_OK;
@@ -462,7 +467,9 @@ alp_status make_plan(const alp_code* code, int64_t units, const alp_params* p, b
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
     optin = 227 * 1024;
   const bool want_gm = p && p->smem_frames_per_sm > 0;
-  if (!want_gm && make_layout_sm(C, pl.L)) {
+  const char* ev = getenv("ALP_SM_D2");
+  const bool sm_d2 = ev && ev[0] == '1';
+  if (!want_gm && make_layout_sm(C, pl.L, sm_d2)) {
     const int wpb = (p && p->warps_per_block > 0) ? p->warps_per_block : 4;
     if ((long long)std::min(wpb, 2) * pl.L.smem_bytes + pl.G.bytes <= optin - 1024) {
       pl.sm = true;
@@ -500,6 +507,7 @@ void alp_default_params(alp_params* p) {
   p->stop_on_lp_failure = 1;
   p->basis_correction = 1;
   p->pcg_forcing = 1e-2;
+  p->pcg_refine = 2;
 }
 
 const char* alp_status_string(alp_status s) {

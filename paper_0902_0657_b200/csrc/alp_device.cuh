@@ -52,7 +52,7 @@ struct Params {
   int variant, precond;
   double sigma, eta, gap_tol, feas_tol, pcg_rel_tol, pcg_forcing, tau_viol, tau_act, tau_cert;
   int alp_max_iter, ipm_max_iter, pcg_max_iter;
-  int stop_on_lp_failure, basis_correction;
+  int stop_on_lp_failure, basis_correction, pcg_refine;
 };
 
 // Device view of the Tanner graph (immutable, shared by all warps; L1/L2 resident).
@@ -84,12 +84,11 @@ __device__ __forceinline__ void stage_graph(const DCode& C, const GraphSmem& G, 
   cp(C.chk_var, G.o_chk_var, C.m * C.dc * 2);
   cp(C.chk_deg, G.o_chk_deg, C.m);
   cp(C.var_chk, G.o_var_chk, C.n * C.dv * 2);
-  cp(C.var_slot, G.o_var_slot, C.n * C.dv);
   cp(C.var_deg, G.o_var_deg, C.n);
   out.chk_var = reinterpret_cast<const uint16_t*>(g + G.o_chk_var);
   out.chk_deg = reinterpret_cast<const uint8_t*>(g + G.o_chk_deg);
   out.var_chk = reinterpret_cast<const uint16_t*>(g + G.o_var_chk);
-  out.var_slot = reinterpret_cast<const uint8_t*>(g + G.o_var_slot);
+  // var_slot stays global: only build_signs reads it, once per LP
   out.var_deg = reinterpret_cast<const uint8_t*>(g + G.o_var_deg);
 }
 
@@ -289,6 +288,7 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.recF = F.recF_();
   F.offB = F.offB_();
   F.offF = F.offF_();
+  if ((L->smask >> RL_D2) & 1u) F.d2 = (double*)(sm + L->soff[RL_D2]);
   F.flip = (uint8_t*)(slot + L->g_flip);
   return;
 #endif
@@ -448,21 +448,28 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   uint32_t* offs = F.S<uint32_t>(L.s_sorth);   // [16 digits][32 lanes]
   const unsigned lt = (1u << F.lane) - 1u;
   int nv = 0;
-  for (int c0 = 0; c0 < C.Q; c0 += 32) {
-    const int c = c0 + F.lane;
-    bool valid = false;
-    uint32_t k = 0;
-    if (c < C.Q) {
-      valid = (c < C.n) ? ((sgnV[c] & 0xf) != 0) : ((sgnC[c - C.n] & PRESENT) != 0);
-      if (valid) k = ~(__float_as_uint(__double2float_rn(d2[c])) & 0x7fffffffu);
+  // compaction of the valid columns with their keys, four 32-column chunks per step so that
+  // the d^2 loads (slot array, L1/L2) of a step are in flight together
+  for (int cb = 0; cb < C.Q; cb += 128) {
+    bool valid[4];
+    uint32_t kk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = cb + 32 * u + F.lane;
+      const int cc = min(c, C.Q - 1);
+      valid[u] = (c < C.Q) && ((cc < C.n) ? ((sgnV[cc] & 0xf) != 0) : ((sgnC[cc - C.n] & PRESENT) != 0));
+      kk[u] = ~(__float_as_uint(__double2float_rn(d2[cc])) & 0x7fffffffu);
     }
-    const unsigned bal = __ballot_sync(FULL, valid);
-    if (valid) {
-      const int at = nv + __popc(bal & lt);
-      kA[at] = k;
-      cA[at] = (uint16_t)c;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned bal = __ballot_sync(FULL, valid[u]);
+      if (valid[u]) {
+        const int at = nv + __popc(bal & lt);
+        kA[at] = kk[u];
+        cA[at] = (uint16_t)(cb + 32 * u + F.lane);
+      }
+      nv += __popc(bal);
     }
-    nv += __popc(bal);
   }
   __syncwarp();
   // LSD radix sort, 8 passes of 4-bit digits.  Lane l owns the contiguous chunk
@@ -529,8 +536,10 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   // first.  Checked in parallel; only then does the serial fix-up below run (e.g. never at
   // IPM iteration 0, where every weight is exactly 1).
   bool tie = false;
-  for (int r = F.lane; r + 1 < nv; r += 32)
-    if (ks[r] == ks[r + 1] && d2[order[r]] < d2[order[r + 1]]) tie = true;
+  for (int r = F.lane; r + 1 < nv; r += 32) {
+    if (ks[r] != ks[r + 1]) continue;   // only equal float keys need the exact weights
+    if (d2[order[r]] < d2[order[r + 1]]) tie = true;
+  }
   if (__any_sync(FULL, tie)) {
     if (F.lane == 0) {
       int r = 0;
@@ -607,29 +616,21 @@ __device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint
       xrR[rr] = (uint16_t)(xrR[rr] ^ R);
       if (nc <= 1) upd = (rr << 1) | (nc == 1 ? 1 : 0);
     }
-    // apply the (<= d_c + 1) bit updates in the owning lanes: shuffles issued back to back,
-    // branch-free set / clear masks per owned word (a column changes at most once per pick)
-    int us[RS];
-#pragma unroll
-    for (int t = 0; t < RS; ++t) us[t] = __shfl_sync(FULL, upd, t);
-    unsigned long long setm[K], clrm[K];
-#pragma unroll
-    for (int kk = 0; kk < K; ++kk) setm[kk] = clrm[kk] = 0ull;
-#pragma unroll
-    for (int t = 0; t < RS; ++t) {
-      const int u = us[t];
+    // apply the DEG1 changes (typically 2-3 of the <= d_c + 1 lanes) in the owning lanes: the
+    // active lanes are enumerated by ballot (warp-uniform loop), one shuffle each
+    unsigned act = __ballot_sync(FULL, upd >= 0);
+    while (act) {
+      const int t = __ffs(act) - 1;
+      act &= act - 1;
+      const int u = __shfl_sync(FULL, upd, t);
       const int rk = u >> 1;
-      const bool mine = (u >= 0) && (((rk >> 6) & 31) == F.lane);
-      const unsigned long long bit = mine ? (1ull << (rk & 63)) : 0ull;
+      if (((rk >> 6) & 31) == F.lane) {
+        const unsigned long long bit = 1ull << (rk & 63);
 #pragma unroll
-      for (int kk = 0; kk < K; ++kk) {
-        const unsigned long long b = ((rk >> 11) == kk) ? bit : 0ull;
-        setm[kk] |= (u & 1) ? b : 0ull;
-        clrm[kk] |= (u & 1) ? 0ull : b;
+        for (int kk = 0; kk < K; ++kk)
+          if ((rk >> 11) == kk) wd[kk] = (u & 1) ? (wd[kk] | bit) : (wd[kk] & ~bit);
       }
     }
-#pragma unroll
-    for (int kk = 0; kk < K; ++kk) wd[kk] = (wd[kk] | setm[kk]) & ~clrm[kk];
     __syncwarp();
   }
 }
@@ -1550,7 +1551,7 @@ __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
 // Status: 0 = the last recursion met pcg_rel_tol (P4), ST_PCG_MAXITER (cap or stall),
 // ST_PCG_BREAKDOWN, ST_PCG_FLOOR (refine mode).  w is read from F.w; dy accumulates in F.dy_().
 __device__ ALP_CALL_PCG PcgResult pcg_solve(const Frame& F, const Params& P, int mode, int nLb, int nLf,
-                                         double itol_rel, bool refine) {
+                                         double itol_rel, int refine) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
   double* hS = F.S<double>(L.s_h);
@@ -1660,7 +1661,7 @@ __device__ ALP_CALL_PCG PcgResult pcg_solve(const Frame& F, const Params& P, int
     // TRUE residual r = w - Q dy: fp64 in the decode (reported), double-double in refine mode
     // (ipm_step_pcg), where it drives the refinement restarts
     double trn;
-    if (refine) {
+    if (refine == 2) {
       trn = sqrt(residual_dd(F, rS));
     } else {
       for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC_()[j] & PRESENT) ? F.dy_()[j] : 0.0;
@@ -1680,6 +1681,26 @@ __device__ ALP_CALL_PCG PcgResult pcg_solve(const Frame& F, const Params& P, int
     res.status = st;
     ALP_TICK(F, CY_PCG, tk);
     if (!refine || st == ST_PCG_BREAKDOWN || !isfinite(trn)) break;
+    if (refine == 1) {
+      // fp64 iterative refinement (round 1): restart from the true residual while it fails
+      // pcg_rel_tol; stop at the fp64 evaluation floor 16 eps || |A| D^2 |A|^T |dy| || (PCG_FLOOR),
+      // or when a restart no longer halves it within 1e3x of that floor
+      if (trn <= tol) break;
+      for (int j = F.lane; j < C.m; j += 32) hS[j] = (F.sgnC_()[j] & PRESENT) ? F.dy_()[j] : 0.0;
+      __syncwarp();
+      spmv<true>(F);
+      double aa = 0.0;
+      for (int j = F.lane; j < C.m; j += 32)
+        if (F.sgnC_()[j] & PRESENT) aa += F.l_()[j] * F.l_()[j];
+      const double floor_est = 16.0 * 2.220446049250313e-16 * sqrt(wsum(aa));
+      if (trn <= floor_est || (trn > 0.5 * prev_trn && trn <= 1e3 * floor_est) || restart == 4) {
+        res.status = (st == 0) ? ST_PCG_FLOOR : st;
+        break;
+      }
+      if (st != 0) break;
+      prev_trn = trn;
+      continue;
+    }
     // Iterative refinement with double-double residuals: restart PCG on Q delta = r (the same
     // preconditioner), dy += delta, while the correction keeps shrinking: stop once
     // ||delta|| <= 1e-13 ||dy||, or ||delta|| no longer halves, or after PCG_REFINE_MAX restarts.

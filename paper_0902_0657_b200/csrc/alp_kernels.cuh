@@ -228,7 +228,7 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
     // dy is admissible because the recovery below keeps every KKT row but the complementarity
     // of the basis columns exact (C-32).
     const double inner = fmin(P.pcg_rel_tol, fmax(1e-14, P.pcg_forcing * mu));
-    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, inner, false);
+    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, inner, 0);
     tk = clock64();
     out.status |= pr.status;
     out.solves += 1;
@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout
           if (io.pcol) io.pcol[s * m + k] = -1;
         }
     }
-    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, P.pcg_rel_tol, true);
+    PcgResult pr = pcg_solve(F, P, mtm ? PC_MTS : PC_NONE, nLb, nLf, P.pcg_rel_tol, P.pcg_refine);
     for (int j = lane; j < m; j += 32) io.dy[s * m + j] = (F.sgnC_()[j] & PRESENT) ? F.dy_()[j] : 0.0;
     if (lane == 0) {
       if (io.iters) io.iters[s] = pr.iters;
