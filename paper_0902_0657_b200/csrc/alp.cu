@@ -137,8 +137,8 @@ size_t make_slot(const DCode& C, Layout& L) {
   L.g_dinvF = g(8 * m);
   L.g_recB = g(2 * m * C.RB);
   L.g_recF = g(2 * m * RF);
-  L.g_offB = g(4 * (m + 2));
-  L.g_offF = g(4 * (m + 2));
+  L.g_offB = g(2 * (m + 2));
+  L.g_offF = g(2 * (m + 2));
   L.g_sgnC = g(2 * m);
   L.g_mask = g(2 * m);
   L.g_hist = g(8 * 256);
@@ -201,10 +201,9 @@ bool make_layout_sm(const DCode& C, Layout& L, bool sm_d2) {
   // D
   const size_t D0 = a;
   rel(RL_L, 8 * m);
-  rel(RL_DY, 8 * m);
   rel(RL_DINVF, 8 * m);
-  rel(RL_OFFB, 4 * (m + 2));
-  rel(RL_OFFF, 4 * (m + 2));
+  rel(RL_OFFB, 2 * (m + 2));
+  rel(RL_OFFF, 2 * (m + 2));
   rel(RL_RECF, 2 * m * (size_t)RF);
   rel(RL_RECB, 2 * m * (size_t)C.RB);
   size_t endD = a;
@@ -302,8 +301,8 @@ Layout make_layout(const DCode& C, int smem_budget) {
   rel_bytes[RL_L] = 8 * m;
   rel_bytes[RL_DY] = 8 * m;
   rel_bytes[RL_DINVF] = 8 * m;
-  rel_bytes[RL_OFFB] = 4 * (m + 2);
-  rel_bytes[RL_OFFF] = 4 * (m + 2);
+  rel_bytes[RL_OFFB] = 2 * (m + 2);
+  rel_bytes[RL_OFFF] = 2 * (m + 2);
   rel_bytes[RL_RECF] = 2 * m * (size_t)RF;
   rel_bytes[RL_RECB] = 2 * m * (size_t)C.RB;
   rel_bytes[RL_D2] = 8 * Q;
@@ -386,8 +385,8 @@ alp_status check_params(const alp_params* p) {
     return fail(ALP_ERR_INVALID_ARG, "iteration caps: 0 <= alp_max_iter <= 255, ipm >= 0, pcg >= 1");
   if (p->pcg_refine < 0 || p->pcg_refine > 2)
     return fail(ALP_ERR_INVALID_ARG, "params.pcg_refine must be 0, 1 or 2");
-  if (p->warps_per_block < 0 || p->warps_per_block > 4 || p->smem_frames_per_sm < 0 || p->smem_frames_per_sm > 32)
-    return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..4, smem_frames_per_sm 0..32");
+  if (p->warps_per_block < 0 || p->warps_per_block > 8 || p->smem_frames_per_sm < 0 || p->smem_frames_per_sm > 32)
+    return fail(ALP_ERR_INVALID_ARG, "params.warps_per_block must be 0..8, smem_frames_per_sm 0..32");
   return ALP_OK;
 }
 
@@ -403,6 +402,10 @@ cudaError_t raise_smem_optin(K kernel, int dev, int bytes) {
   if (e == cudaSuccess) done.emplace_back(key, dev);
   return e;
 }
+
+// relocation mask of the shared-memory mode's fixed layout (make_layout_sm)
+constexpr unsigned SM_FIXED_MASK = (1u << RL_SGNC) | (1u << RL_SGNV) | (1u << RL_L) | (1u << RL_DINVF) |
+                                   (1u << RL_OFFB) | (1u << RL_OFFF) | (1u << RL_RECF) | (1u << RL_RECB);
 
 struct LaunchCfg {
   int wpb, grid, smem_block;
@@ -420,7 +423,9 @@ alp_status plan_launch(K kernel, const Layout& L, int graph_bytes, long long uni
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   smem_optin -= 1024;   // static shared memory of the kernels (code / layout descriptors)
-  int wpb = (p && p->warps_per_block > 0) ? p->warps_per_block : 4;
+  // frames (warps) per CTA: the caller's choice, else 4 for the generic mode and, for the
+  // shared-memory mode (one CTA per SM), as many windows as fit (<= 8)
+  int wpb = (p && p->warps_per_block > 0) ? p->warps_per_block : (L.win_global || L.smask != SM_FIXED_MASK ? 4 : 8);
   while (wpb > 1 && (long long)wpb * L.smem_bytes + graph_bytes > smem_optin) --wpb;
   if ((long long)wpb * L.smem_bytes + graph_bytes > smem_optin)
     return fail(ALP_ERR_UNSUPPORTED, "per-frame shared memory " + std::to_string(L.smem_bytes) +
@@ -470,8 +475,9 @@ alp_status make_plan(const alp_code* code, int64_t units, const alp_params* p, b
   const char* ev = getenv("ALP_SM_D2");
   const bool sm_d2 = ev && ev[0] == '1';
   if (!want_gm && make_layout_sm(C, pl.L, sm_d2)) {
-    const int wpb = (p && p->warps_per_block > 0) ? p->warps_per_block : 4;
-    if ((long long)std::min(wpb, 2) * pl.L.smem_bytes + pl.G.bytes <= optin - 1024) {
+    // worth it when at least 4 windows fit a CTA (C1, C2; measured: config 5's 92 KB windows run
+    // faster in the generic mode, 151 k vs 103 k systems/s)
+    if (4LL * pl.L.smem_bytes + pl.G.bytes <= optin - 1024) {
       pl.sm = true;
       return step ? plan_launch(sm::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
                   : plan_launch(sm::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
@@ -507,7 +513,7 @@ void alp_default_params(alp_params* p) {
   p->stop_on_lp_failure = 1;
   p->basis_correction = 1;
   p->pcg_forcing = 1e-2;
-  p->pcg_refine = 2;
+  p->pcg_refine = 1;
 }
 
 const char* alp_status_string(alp_status s) {

@@ -198,7 +198,7 @@ struct Frame {
   double *x, *z, *d2, *v, *y, *dy, *l, *w, *u, *b, *dinvF, *rb, *rc;
   uint16_t* pcolR;  // [m]: pivot column of pivot row R (0..n+m-1), NONE16 if R is not a pivot
   uint16_t *recB, *recF;  // sweep programs (u16 records, see build_precond)
-  int *offB, *offF;
+  uint16_t *offB, *offF;   // level offsets (u16: <= p + 1 <= 32768)
   uint16_t* sgnC;  // [m]: bit t <-> coefficient of x_{N(j)[t]} is -1; bit 15 <-> row present
   uint16_t* mask;  // [m]: cut pool (include/alp.h mask word)
   unsigned long long* hist;  // [alp_max_iter + 1] pool hashes of the LPs solved (C-12)
@@ -218,12 +218,12 @@ struct Frame {
   __device__ __forceinline__ uint16_t* sgnC_() const { return W_<uint16_t>(o_sgnC); }
   __device__ __forceinline__ uint8_t* sgnV_() const { return W_<uint8_t>(o_sgnV); }
   __device__ __forceinline__ double* l_() const { return W_<double>(o_l); }
-  __device__ __forceinline__ double* dy_() const { return W_<double>(o_dy); }
+  __device__ __forceinline__ double* dy_() const { return dy; }   // slot (global): frees 8m bytes
   __device__ __forceinline__ double* dinvF_() const { return W_<double>(o_dinvF); }
   __device__ __forceinline__ uint16_t* recB_() const { return W_<uint16_t>(o_recB); }
   __device__ __forceinline__ uint16_t* recF_() const { return W_<uint16_t>(o_recF); }
-  __device__ __forceinline__ int* offB_() const { return W_<int>(o_offB); }
-  __device__ __forceinline__ int* offF_() const { return W_<int>(o_offF); }
+  __device__ __forceinline__ uint16_t* offB_() const { return W_<uint16_t>(o_offB); }
+  __device__ __forceinline__ uint16_t* offF_() const { return W_<uint16_t>(o_offF); }
 #else
   template <class T>
   __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(sm + off); }
@@ -234,8 +234,8 @@ struct Frame {
   __device__ __forceinline__ double* dinvF_() const { return dinvF; }
   __device__ __forceinline__ uint16_t* recB_() const { return recB; }
   __device__ __forceinline__ uint16_t* recF_() const { return recF; }
-  __device__ __forceinline__ int* offB_() const { return offB; }
-  __device__ __forceinline__ int* offF_() const { return offF; }
+  __device__ __forceinline__ uint16_t* offB_() const { return offB; }
+  __device__ __forceinline__ uint16_t* offF_() const { return offF; }
 #endif
 };
 
@@ -259,8 +259,8 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.dinvF = (double*)(slot + L->g_dinvF);
   F.recB = (uint16_t*)(slot + L->g_recB);
   F.recF = (uint16_t*)(slot + L->g_recF);
-  F.offB = (int*)(slot + L->g_offB);
-  F.offF = (int*)(slot + L->g_offF);
+  F.offB = (uint16_t*)(slot + L->g_offB);
+  F.offF = (uint16_t*)(slot + L->g_offF);
   F.sgnC = (uint16_t*)(slot + L->g_sgnC);
   F.mask = (uint16_t*)(slot + L->g_mask);
   F.hist = (unsigned long long*)(slot + L->g_hist);
@@ -273,7 +273,6 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.o_sgnC = L->soff[RL_SGNC];
   F.o_sgnV = L->soff[RL_SGNV];
   F.o_l = L->soff[RL_L];
-  F.o_dy = L->soff[RL_DY];
   F.o_dinvF = L->soff[RL_DINVF];
   F.o_recB = L->soff[RL_RECB];
   F.o_recF = L->soff[RL_RECF];
@@ -282,7 +281,6 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.sgnC = F.sgnC_();
   F.sgnV = F.sgnV_();
   F.l = F.l_();
-  F.dy = F.dy_();
   F.dinvF = F.dinvF_();
   F.recB = F.recB_();
   F.recF = F.recF_();
@@ -294,8 +292,8 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
 #endif
   F.recB = (uint16_t*)rel_ptr(L, slot, sm, RL_RECB, L->g_recB);
   F.recF = (uint16_t*)rel_ptr(L, slot, sm, RL_RECF, L->g_recF);
-  F.offB = (int*)rel_ptr(L, slot, sm, RL_OFFB, L->g_offB);
-  F.offF = (int*)rel_ptr(L, slot, sm, RL_OFFF, L->g_offF);
+  F.offB = (uint16_t*)rel_ptr(L, slot, sm, RL_OFFB, L->g_offB);
+  F.offF = (uint16_t*)rel_ptr(L, slot, sm, RL_OFFF, L->g_offF);
   F.dinvF = (double*)rel_ptr(L, slot, sm, RL_DINVF, L->g_dinvF);
   F.sgnC = (uint16_t*)rel_ptr(L, slot, sm, RL_SGNC, L->g_sgnC);
   F.sgnV = (uint8_t*)rel_ptr(L, slot, sm, RL_SGNV, L->g_sgnV);
@@ -616,21 +614,30 @@ __device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint
       xrR[rr] = (uint16_t)(xrR[rr] ^ R);
       if (nc <= 1) upd = (rr << 1) | (nc == 1 ? 1 : 0);
     }
-    // apply the DEG1 changes (typically 2-3 of the <= d_c + 1 lanes) in the owning lanes: the
-    // active lanes are enumerated by ballot (warp-uniform loop), one shuffle each
-    unsigned act = __ballot_sync(FULL, upd >= 0);
-    while (act) {
-      const int t = __ffs(act) - 1;
-      act &= act - 1;
-      const int u = __shfl_sync(FULL, upd, t);
-      const int rk = u >> 1;
-      if (((rk >> 6) & 31) == F.lane) {
-        const unsigned long long bit = 1ull << (rk & 63);
+    // apply the (<= d_c + 1) bit updates in the owning lanes: shuffles issued back to back,
+    // branch-free set / clear masks per owned word (a column changes at most once per pick;
+    // measured faster than enumerating the active lanes by ballot)
+    int us[RS];
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk)
-          if ((rk >> 11) == kk) wd[kk] = (u & 1) ? (wd[kk] | bit) : (wd[kk] & ~bit);
+    for (int t = 0; t < RS; ++t) us[t] = __shfl_sync(FULL, upd, t);
+    unsigned long long setm[K], clrm[K];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) setm[kk] = clrm[kk] = 0ull;
+#pragma unroll
+    for (int t = 0; t < RS; ++t) {
+      const int u = us[t];
+      const int rk = u >> 1;
+      const bool mine = (u >= 0) && (((rk >> 6) & 31) == F.lane);
+      const unsigned long long bit = mine ? (1ull << (rk & 63)) : 0ull;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const unsigned long long b = ((rk >> 11) == kk) ? bit : 0ull;
+        setm[kk] |= (u & 1) ? b : 0ull;
+        clrm[kk] |= (u & 1) ? 0ull : b;
       }
     }
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) wd[kk] = (wd[kk] | setm[kk]) & ~clrm[kk];
     __syncwarp();
   }
 }
@@ -1043,7 +1050,7 @@ __device__ int compute_levels(const Frame& F, int p, uint16_t* lv) {
 
 // Deterministic counting sort of pivots by level: lv[k] (level) is replaced by the slot of
 // pivot k in level order; off[0..nL] (global) receives the level boundaries.
-__device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* off) {
+__device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, uint16_t* off) {
   int* hist = F.S<int>(F.L->s_hist);
   int* cur = F.S<int>(F.L->s_cur);
   for (int l = F.lane; l <= nL; l += 32) hist[l] = 0;
@@ -1061,12 +1068,12 @@ __device__ void level_slots(const Frame& F, int p, int nL, uint16_t* lv, int* of
       if (F.lane >= o) incl += t;
     }
     if (l < nL) {
-      off[l] = carry + incl - hv;
+      off[l] = (uint16_t)(carry + incl - hv);
       cur[l] = carry + incl - hv;
     }
     carry += __shfl_sync(FULL, incl, 31);
   }
-  if (F.lane == 0) off[nL] = carry;
+  if (F.lane == 0) off[nL] = (uint16_t)carry;
   __syncwarp();
   const unsigned lt = (1u << F.lane) - 1u;
   for (int b0 = 0; b0 < p; b0 += 32) {
@@ -1186,8 +1193,8 @@ __device__ void write_pivots(const Frame& F, int p, int* rows, int* cols) {
 // level).
 struct OffReg {
   int a, b;
-  const int* mem;
-  __device__ __forceinline__ void load(const int* off, int nL, int lane) {
+  const uint16_t* mem;
+  __device__ __forceinline__ void load(const uint16_t* off, int nL, int lane) {
     mem = off;
     a = (lane <= nL) ? off[lane] : 0;
     b = (32 + lane <= nL) ? off[32 + lane] : 0;
@@ -1604,13 +1611,29 @@ __device__ ALP_CALL_PCG PcgResult pcg_solve(const Frame& F, const Params& P, int
         double* __restrict__ dyp = F.dy_();
         const double* __restrict__ lp = F.l_();
         const uint16_t* __restrict__ sc = F.sgnC_();
-#pragma unroll 4
-        for (int j = F.lane; j < C.m; j += 32) {
-          if (!(sc[j] & PRESENT)) continue;
-          dyp[j] += alpha * hS[j];             // line 8
-          const double r = rS[j] - alpha * lp[j];   // line 9
-          rS[j] = r;
-          acc += r * r;
+        // four rows per lane per step, all loads first (dy lives in the slot: its L1/L2 round
+        // trips overlap)
+        for (int j0 = F.lane; j0 < C.m; j0 += 128) {
+          double dv[4], hv[4], lv[4], rv[4];
+          bool pr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = min(j0 + 32 * u, C.m - 1);
+            pr[u] = (j0 + 32 * u < C.m) && (sc[j] & PRESENT);
+            dv[u] = dyp[j];
+            hv[u] = hS[j];
+            lv[u] = lp[j];
+            rv[u] = rS[j];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (!pr[u]) continue;
+            const int j = j0 + 32 * u;
+            dyp[j] = dv[u] + alpha * hv[u];          // line 8
+            const double r = rv[u] - alpha * lv[u];  // line 9
+            rS[j] = r;
+            acc += r * r;
+          }
         }
       }
       __syncwarp();

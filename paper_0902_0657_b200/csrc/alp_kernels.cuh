@@ -548,7 +548,7 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
 #ifndef ALP_MINB
 #define ALP_MINB 1
 #endif
-__global__ void __launch_bounds__(128, ALP_MINB) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
+__global__ void __launch_bounds__(256, ALP_MINB) alp_decode_kernel(DCode C, Params P, Layout L, GraphSmem G,
                                                         char* slots,
                                                         const double* __restrict__ llr,
                                                         long long n_frames, DecodeOut O,
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(128, ALP_MINB) alp_decode_kernel(DCode C, Para
   Frame F;
   char* slot = slots + gw * L.slot_bytes;
   frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
-  __shared__ long long s_cyc[4][8];   // phase clocks in shared memory (a global RMW per tick
+  __shared__ long long s_cyc[8][8];   // phase clocks in shared memory (a global RMW per tick
   F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
   while (true) {
     long long f = 0;
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(128, ALP_MINB) alp_decode_kernel(DCode C, Para
 
 
 // Isolated step solve (eq.`Delta y` P:479) per system: signs, D^2, Alg. 7, PCG.
-__global__ void __launch_bounds__(128) pcg_step_kernel(DCode C, Params P, Layout L, GraphSmem G,
+__global__ void __launch_bounds__(256, 1) pcg_step_kernel(DCode C, Params P, Layout L, GraphSmem G,
                                                       char* slots, long long n_sys, StepIO io,
                                                       unsigned long long* counter) {
   extern __shared__ __align__(16) char smem[];
