@@ -1381,13 +1381,17 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, co
   ALP_GL_SM(d2s_);
   double* __restrict__ lout = F.l_();
   const int m = C.m, dc = C.dc;
+#ifndef ALP_SPMV_UC
+#define ALP_SPMV_UC 2
+#endif
+  constexpr int UC = ALP_SPMV_UC;   // checks per lane per step
   double hl = 0.0;
-  for (int j0 = F.lane; j0 < m; j0 += 64) {
-    uint16_t sc[2];
-    double hj[2], d2s[2];
-    int in[2][DCT];
+  for (int j0 = F.lane; j0 < m; j0 += 32 * UC) {
+    uint16_t sc[UC];
+    double hj[UC], d2s[UC];
+    int in[UC][DCT];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < UC; ++u) {
       const int j = j0 + 32 * u;
       const bool ok = j < m;
       sc[u] = ok ? sgnC[j] : (uint16_t)0;
@@ -1397,9 +1401,9 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, co
 #pragma unroll
       for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)chk_var[j * dc + t] : -1;
     }
-    double acc[2];
+    double acc[UC];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < UC; ++u) {
       const double ds = d2s[u] * (ABS ? fabs(hj[u]) : hj[u]);
       acc[u] = ds;
 #pragma unroll
@@ -1413,7 +1417,7 @@ __device__ __forceinline__ double spmv_checks(const Frame& F, const DCode& C, co
       if (sc[u] & PRESENT) hl += hj[u] * ds;
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < UC; ++u) {
       const int j = j0 + 32 * u;
       if (j < m && (sc[u] & PRESENT)) lout[j] = acc[u];
     }
@@ -1437,7 +1441,10 @@ __device__ ALP_HEAVY double spmv(const Frame& F) {
   // variable pass, U variables per lane per step: all their index / sign / weight loads are
   // issued before any gather, and all gathers before any store (the shared-memory store of
   // t would otherwise block hoisting the next variable's loads)
-  constexpr int U = 2;
+#ifndef ALP_SPMV_UV
+#define ALP_SPMV_UV 2
+#endif
+  constexpr int U = ALP_SPMV_UV;   // variables per lane per step
   for (int i0 = F.lane; i0 < n; i0 += 32 * U) {
     uint8_t sv[U];
     double dv[U];
