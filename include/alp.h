@@ -112,7 +112,9 @@ typedef struct {
 typedef struct {
   int32_t variant;        /* 0 = MALP-A (Alg. 3), 1 = MALP-B                         */
   int32_t precond;        /* 0 = column-wise greedy MTS (Alg. 7, default), 1 = none (plain CG,
-                             P:511), 2 = row-wise greedy MTS with diagonal expansion (Alg. 8) */
+                             P:511), 2 = row-wise greedy MTS with diagonal expansion (Alg. 8),
+                             3 = incremental greedy MTS (Alg. 6 with the Triangulation Step,
+                             Alg. 5; O(q) triangulations per build: a reference variant)  */
   double sigma;           /* centering: mu = sigma * x^T z / q (eq.`update mu`, C-5)   0.1    */
   double eta;             /* step damping of the ratio test (C-6)                0.99   */
   double gap_tol;         /* stop: x^T z <= gap_tol * (1 + |c^T x|) (C-8)               1e-9   */
@@ -221,6 +223,15 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
  * alp_decode appends one record per Newton-step solve (order unspecified, records beyond
  * capacity dropped).  NULL disables.  Process-wide; not thread safe; not for production. */
 alp_status alp_debug_trace(void* records, int32_t capacity);
+
+/* Launch plan of alp_decode (step = 0) or ipm_step_pcg (step = 1) for `units` frames / systems
+ * on the current device (engineering introspection, used by bench.py to report the residency).
+ * info[0] = 1 for the shared-memory window mode, 0 for the generic mode; info[1] = frames
+ * (warps) per CTA; info[2] = grid (CTAs); info[3] = shared-memory bytes per frame window;
+ * info[4] = shared-memory bytes per CTA; info[5] = global slot bytes per warp.  info: HOST
+ * pointer to 6 int32, owned by the caller.  Errors as for alp_decode_workspace_bytes. */
+alp_status alp_launch_info(const alp_code* code, int64_t units, const alp_params* params, int32_t step,
+                           int32_t* info);
 
 /* Kernel launches enqueued by the last successful alp_decode / ipm_step_pcg on this thread. */
 int32_t alp_last_launch_count(void);

@@ -5,7 +5,7 @@ C ABI.  This package is its thin Python binding (api), the in-tree build (build)
 the multi-GPU sharding helpers (dist).  It never imports `oracle/`.
 """
 from .api import (AlpError, Code, DecodeResult, StepResult, Workspace, decode, decode_host,
-                  default_params, ipm_step_pcg, last_launch_count, lib, STATS_DTYPE)
+                  default_params, ipm_step_pcg, last_launch_count, launch_info, lib, STATS_DTYPE)
 
 __all__ = ["AlpError", "Code", "DecodeResult", "StepResult", "Workspace", "decode", "decode_host",
-           "default_params", "ipm_step_pcg", "last_launch_count", "lib", "STATS_DTYPE"]
+           "default_params", "ipm_step_pcg", "last_launch_count", "launch_info", "lib", "STATS_DTYPE"]

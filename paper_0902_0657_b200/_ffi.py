@@ -60,6 +60,7 @@ SIGNATURES = {
     "ipm_step_pcg": (C.c_int, [P, C.c_int64, P, P, P, P, P, P, P, P, P, P, P, C.c_size_t,
                                C.POINTER(AlpParams), P]),
     "alp_last_launch_count": (C.c_int32, []),
+    "alp_launch_info": (C.c_int, [P, C.c_int64, C.POINTER(AlpParams), C.c_int32, P]),
     "alp_debug_trace": (C.c_int, [P, C.c_int32]),
     "alp_status_string": (C.c_char_p, [C.c_int]),
     "alp_last_error": (C.c_char_p, []),
@@ -68,6 +69,7 @@ SIGNATURES = {
 }
 
 _lib = None
+OPTIONAL = ("alp_launch_info",)
 
 
 def load(path: str | None = None):
@@ -82,6 +84,8 @@ def load(path: str | None = None):
                           "(or __graft_entry__.build()); there is no CPU fallback")
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if name in OPTIONAL and path != LIB_PATH and not hasattr(lib, name):
+            continue   # an older tuning build under ALP_LIB (introspection calls only)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -234,3 +234,13 @@ def ipm_step_pcg(code: Code, masks: torch.Tensor, d: torch.Tensor, r: torch.Tens
 
 def last_launch_count() -> int:
     return int(lib().alp_last_launch_count())
+
+
+def launch_info(code: "Code", units: int, params=None, step: bool = False) -> dict:
+    """Launch plan the library would use (alp_launch_info): window mode, frames per CTA, grid,
+    shared-memory bytes per frame / per CTA, slot bytes per warp."""
+    info = (C.c_int32 * 6)()
+    pp = C.byref(params) if params is not None else None
+    _check(lib().alp_launch_info(code.handle, int(units), pp, 1 if step else 0, C.addressof(info)))
+    return dict(smem_mode=bool(info[0]), frames_per_cta=info[1], grid=info[2], smem_per_frame=info[3],
+                smem_per_cta=info[4], slot_bytes=info[5])

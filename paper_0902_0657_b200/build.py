@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "alp.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "alp_device.cuh"), os.path.join(ROOT, "include", "alp.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", n) for n in ("alp_device.cuh", "alp_kernels.cuh")] + [os.path.join(ROOT, "include", "alp.h")]
 OUT = os.path.join(HERE, "libalp.so")
 
 NVCC_FLAGS = [

@@ -130,7 +130,6 @@ size_t make_slot(const DCode& C, Layout& L) {
   L.g_v = g(8 * Q);
   L.g_y = g(8 * m);
   L.g_dy = g(8 * m);
-  L.g_l = g(8 * m);
   L.g_w = g(8 * m);
   L.g_u = g(8 * n);
   L.g_b = g(8 * m);
@@ -147,19 +146,21 @@ size_t make_slot(const DCode& C, Layout& L) {
   L.g_rb = g(8 * m);
   L.g_rc = g(8 * Q);
   L.g_pcol = g(2 * m);
+  L.g_r = g(8 * m);
   L.slot_bytes = (long long)al(o, 256);
   return o;
 }
 
 // Window layout of the shared-memory mode (kernel alp::sm::*): one fixed per-frame window,
-//   P: PCG vectors h, r, f, z [m] (t [n] over f, z when it fits, else after them); the build's
-//      late arrays (pos, pcol, prow, lvB, lvF, poc, hist, cur) overlay P;
-//   sgnC [m], sgnV [n];
-//   D: l, dy, dinvF [m], level offsets, sweep records (all dead while the preconditioner is
-//      being built); the build's early arrays (order, radix buffers / rank, cnt, xr, DEG1
-//      bitmap, row ranks) overlay D.
-// d^2, w and the IPM arrays stay in the slot (L1/L2).  Returns false when the late arrays do
-// not fit P (then the generic mode is used).
+//   S: sgnC [m], sgnV [n] (live throughout);
+//   P: PCG vectors h, r, dy [m] and fz [max(m, n)] (f, z in place; t of the SpMV over it);
+//   D: the sweep programs: back / forward records, dinvF, level offsets.
+// The preconditioner build overlays P and D (both dead while it runs): the column sort's radix
+// buffers from the start of P with `order` after them; the peel's pos / pcol / prow at the start
+// of P and its rank / count / XOR / bitmap / row-rank arrays after them; the post-peel arrays
+// (levels, pivot-of-column map, level histograms) after pos / pcol / prow, inside P (the
+// records in D are written from them).  d^2, w and the IPM arrays stay in the slot (L1/L2).
+// Returns false when the post-peel arrays do not fit P (then the generic mode is used).
 bool make_layout_sm(const DCode& C, Layout& L, bool sm_d2) {
   const size_t n = C.n, m = C.m, Q = C.Q;
   make_slot(C, L);
@@ -171,25 +172,6 @@ bool make_layout_sm(const DCode& C, Layout& L, bool sm_d2) {
     a += al(bytes, 16);
     return (int)r;
   };
-  // P
-  L.s_h = s(8 * m);
-  L.s_r = s(8 * m);
-  L.s_f = s(8 * m);
-  L.s_z = s(8 * m);
-  size_t endP = a;
-  if (8 * n <= endP - L.s_f) L.s_t = L.s_f;
-  else { L.s_t = s(8 * n); endP = a; }
-  a = 0;   // late build arrays over P
-  L.s_pos = s(2 * m);
-  L.s_pcol = s(2 * m);
-  L.s_prow = s(2 * m);
-  L.s_lvB = s(2 * m);
-  L.s_lvF = s(2 * m);
-  L.s_poc = s(2 * Q);
-  L.s_hist = s(4 * (m + 2));
-  L.s_cur = s(4 * (m + 2));
-  if (a > endP) return false;
-  a = endP;
   L.smask = 0;
   auto rel = [&](int k, size_t bytes) {
     L.smask |= 1u << k;
@@ -197,31 +179,53 @@ bool make_layout_sm(const DCode& C, Layout& L, bool sm_d2) {
   };
   rel(RL_SGNC, 2 * m);
   rel(RL_SGNV, n);
-  if (sm_d2) rel(RL_D2, 8 * Q);   // d^2 too (fewer frames per SM; tuning)
+  const size_t S0 = a;
+  // P
+  L.s_h = s(8 * m);
+#ifdef ALP_SM_R_SLOT
+  L.s_r = -1;   // r lives in the slot (tuning variant)
+#else
+  L.s_r = s(8 * m);
+#endif
+  rel(RL_DY, 8 * m);
+  L.s_fz = s(8 * std::max(m, n));
+  const size_t endP = a;
   // D
-  const size_t D0 = a;
-  rel(RL_L, 8 * m);
+  rel(RL_RECB, 2 * m * (size_t)C.RB);
+  rel(RL_RECF, 2 * m * (size_t)RF);
   rel(RL_DINVF, 8 * m);
   rel(RL_OFFB, 2 * (m + 2));
   rel(RL_OFFF, 2 * (m + 2));
-  rel(RL_RECF, 2 * m * (size_t)RF);
-  rel(RL_RECB, 2 * m * (size_t)C.RB);
-  size_t endD = a;
-  a = D0;   // early build arrays over D
-  L.s_order = s(2 * Q);
-  const size_t E0 = a;
-  L.s_sortk = (int)E0;
-  L.s_sorth = (int)(E0 + al(12 * Q, 16));
-  const size_t endSort = E0 + al(12 * Q, 16) + 2048;
-  a = E0;
+  if (sm_d2) rel(RL_D2, 8 * Q);   // d^2 too (fewer frames per SM; tuning)
+  const size_t endD = a;
+  // build, post-peel: pos / pcol / prow, then the level arrays, inside P
+  a = S0;
+  L.s_pos = s(2 * m);
+  L.s_pcol = s(2 * m);
+  L.s_prow = s(2 * m);
+  const size_t L0 = a;
+  L.s_lvB = s(2 * m);
+  L.s_lvF = s(2 * m);
+  L.s_poc = s(2 * Q);
+  L.s_hist = s(4 * (m + 2));
+  L.s_cur = s(4 * (m + 2));
+  if (a > endP) return false;
+  // build, peel: after pos / pcol / prow
+  a = L0;
   L.s_rank = s(2 * Q);
   L.s_cnt = s(Q);
   L.s_xr = s(2 * Q);
   L.s_bm = s(8 * (size_t)C.W);
   L.RS = (C.dcr + 1 <= 8) ? 8 : 16;
   L.s_rrank = s(2 * m * (size_t)L.RS);
-  const size_t endE = std::max(a, endSort);
-  L.smem_bytes = (int)al(std::max(endD, endE), 128);
+  const size_t endPeel = a;
+  // build, sort: radix buffers kA/kB u32[Q], cA/cB u16[Q] and the digit table from S0; the
+  // ranked column order after both the sort buffers and the peel arrays
+  L.s_sortk = (int)S0;
+  L.s_sorth = (int)(S0 + al(12 * Q, 16));
+  a = std::max(S0 + al(12 * Q, 16) + 2048, endPeel);
+  L.s_order = s(2 * Q);
+  L.smem_bytes = (int)al(std::max(endD, a), 128);
   return true;
 }
 
@@ -266,19 +270,12 @@ Layout make_layout(const DCode& C, int smem_budget) {
     L.s_cur = (int)(end_peel + al(4 * (m + 2), 16));
     end_peel += need;
   }
-  // PCG phase
+  // PCG phase: h, r [m], fz [max(m, n)] (f and z in place; t over it)
   a = 0;
   L.s_h = s(8 * m);
   L.s_r = s(8 * m);
-  L.s_f = s(8 * m);
-  L.s_z = s(8 * m);
+  L.s_fz = s(8 * std::max(m, n));
   size_t end_pcg = a;
-  if (8 * n <= end_pcg - L.s_f) {
-    L.s_t = L.s_f;  // t (per variable) aliases f and z (dead during the SpMV)
-  } else {
-    L.s_t = s(8 * n);
-    end_pcg = a;
-  }
   size_t tot = al(std::max(s_sort, std::max(end_peel, end_pcg)), 16);
   L.win_global = 0;
   L.g_win = 0;
@@ -293,12 +290,11 @@ Layout make_layout(const DCode& C, int smem_budget) {
     return L;
   }
   // Relocate the arrays the PCG loop touches every iteration into the shared window, by
-  // priority (sign tables, l, dy, sweep program, D^2, w), while the window fits the budget.
+  // priority (sign tables, dy, sweep programs, D^2, w), while the window fits the budget.
   L.smask = 0;
   size_t rel_bytes[RL_N];
   rel_bytes[RL_SGNC] = 2 * m;
   rel_bytes[RL_SGNV] = n;
-  rel_bytes[RL_L] = 8 * m;
   rel_bytes[RL_DY] = 8 * m;
   rel_bytes[RL_DINVF] = 8 * m;
   rel_bytes[RL_OFFB] = 2 * (m + 2);
@@ -377,8 +373,8 @@ Params make_params(const alp_params* p) {
 alp_status check_params(const alp_params* p) {
   if (!p) return ALP_OK;
   if (p->variant < 0 || p->variant > 1) return fail(ALP_ERR_INVALID_ARG, "params.variant must be 0 or 1");
-  if (p->precond < 0 || p->precond > 2)
-    return fail(ALP_ERR_INVALID_ARG, "params.precond must be 0 (Alg. 7), 1 (plain CG) or 2 (Alg. 8)");
+  if (p->precond < 0 || p->precond > 3)
+    return fail(ALP_ERR_INVALID_ARG, "params.precond must be 0 (Alg. 7), 1 (plain CG), 2 (Alg. 8) or 3 (Alg. 6)");
   if (!(p->sigma > 0 && p->sigma < 1) || !(p->eta > 0 && p->eta < 1))
     return fail(ALP_ERR_INVALID_ARG, "params.sigma and params.eta must lie in (0,1)");
   if (p->alp_max_iter < 0 || p->alp_max_iter > 255 || p->ipm_max_iter < 0 || p->pcg_max_iter < 1)
@@ -404,7 +400,7 @@ cudaError_t raise_smem_optin(K kernel, int dev, int bytes) {
 }
 
 // relocation mask of the shared-memory mode's fixed layout (make_layout_sm)
-constexpr unsigned SM_FIXED_MASK = (1u << RL_SGNC) | (1u << RL_SGNV) | (1u << RL_L) | (1u << RL_DINVF) |
+constexpr unsigned SM_FIXED_MASK = (1u << RL_SGNC) | (1u << RL_SGNV) | (1u << RL_DY) | (1u << RL_DINVF) |
                                    (1u << RL_OFFB) | (1u << RL_OFFF) | (1u << RL_RECF) | (1u << RL_RECB);
 
 struct LaunchCfg {
@@ -537,6 +533,23 @@ const char* alp_build_info(void) {
 }
 
 int32_t alp_last_launch_count(void) { return g_last_launches; }
+
+alp_status alp_launch_info(const alp_code* code, int64_t units, const alp_params* params, int32_t step,
+                           int32_t* info) {
+  if (!code || !info || units < 0) return fail(ALP_ERR_INVALID_ARG, "code / info NULL or units < 0");
+  alp_status ps = check_params(params);
+  if (ps != ALP_OK) return ps;
+  Plan pl;
+  alp_status st = make_plan(code, units, params, step != 0, pl);
+  if (st != ALP_OK) return st;
+  info[0] = pl.sm ? 1 : 0;
+  info[1] = pl.cfg.wpb;
+  info[2] = pl.cfg.grid;
+  info[3] = pl.L.smem_bytes;
+  info[4] = pl.cfg.smem_block;
+  info[5] = (int32_t)pl.L.slot_bytes;
+  return ALP_OK;
+}
 
 alp_status alp_debug_trace(void* records, int32_t capacity) {
   void* ptr = records;

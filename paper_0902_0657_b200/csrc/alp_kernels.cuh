@@ -216,11 +216,11 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
     else ipm_rows_w<DCMAX>(C, lane, SC, W, V);
     __syncwarp();
     int nLb = 0, nLf = 0;
-    const bool mtm = (P.precond == 0 || P.precond == 2);   // MTS-preconditioned PCG
+    const bool mtm = (P.precond != 1);   // MTS-preconditioned PCG (Alg. 7, 8 or 6)
     ALP_TICK(F, CY_IPM, tk);
     // the Alg. 7 triangular set is both the PCG preconditioner (precond = 0) and the basis of
     // the step's feasibility correction (C-32), so plain CG builds it too when that is on
-    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf, P.precond == 2 ? 2 : 0);
+    if (mtm || P.basis_correction) build_precond(F, p, nLb, nLf, P.precond == 1 ? 0 : P.precond);
     ALP_TICK(F, CY_BUILD, tk);
     // inexact-Newton forcing term (R-1): the dual step needs A^T dy accurate to well
     // below z ~ mu on the basic columns, so late in the IPM the recursion aims at
@@ -302,8 +302,8 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
     }
     __syncwarp();
     if (P.basis_correction && nLb > 0) {
-      double* rS = F.S<double>(F.L->s_r);
-      const double* fS = F.S<double>(F.L->s_f);
+      double* rS = F.r_();
+      double* fS = F.fz_();
       for (int j = lane; j < m; j += 32) {
         uint16_t s = SC[j];
         double rho = 0.0;
@@ -319,10 +319,11 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
         rS[j] = rho;
       }
       __syncwarp();
-      back_sweep(F, nLb);   // f = A_M^-1 rho, f_R = component of row R's pivot column
+      back_sweep(F, nLb, rS, fS);   // f = A_M^-1 rho, f_R = component of row R's pivot column
       __syncwarp();
+      const uint16_t* pcolR = F.pcolR_();
       for (int j = lane; j < m; j += 32) {
-        const uint16_t c = F.pcolR[j];
+        const uint16_t c = pcolR[j];
         if (c != NONE16) V[c] += fS[j];
       }
       __syncwarp();
@@ -614,7 +615,7 @@ __global__ void __launch_bounds__(256, 1) pcg_step_kernel(DCode C, Params P, Lay
     for (int j = lane; j < m; j += 32) F.w[j] = (F.sgnC_()[j] & PRESENT) ? io.r[s * m + j] : 0.0;
     __syncwarp();
     int nLb = 0, nLf = 0;
-    const bool mtm = (P.precond == 0 || P.precond == 2) && p > 0;
+    const bool mtm = (P.precond != 1) && p > 0;
     if (mtm) build_precond(F, p, nLb, nLf, P.precond);
     if ((io.prow || io.pcol)) {
       if (mtm) write_pivots(F, p, io.prow ? io.prow + s * m : nullptr, io.pcol ? io.pcol + s * m : nullptr);

@@ -261,6 +261,39 @@ def test_rowwise_mts_matches_oracle_alg8():
     _check_rowwise(code5, sy5.masks, sy5.d, sy5.r)
 
 
+def _check_incremental(code, masks, d, r, flip=None):
+    """Alg. 6 on the GPU (precond = 3): the pivot sequence, read back in pick order, equals the
+    reversed lower-triangular Triangulation Step ordering of the oracle's mts_incremental."""
+    from oracle.precond import mts_incremental
+    out = _run(code, masks, d, r, flip, precond=3)
+    for s in range(masks.shape[0]):
+        A, rows = dense_step_matrix(code, masks[s], None if flip is None else flip[s])
+        if not rows:
+            continue
+        w2 = step_weights(code, d[s], rows)
+        col, row = mts_incremental(A, w2)
+        p = len(rows)
+        assert len(col) == p, "Alg. 6 must reach |M| = p (P:656)"
+        exp_rows = [rows[rw] for rw in row][::-1]          # stored reversed (upper triangular)
+        exp_cols = [oracle_col_to_gpu(code, rows, c) for c in col][::-1]
+        assert list(out["prow"][s][:p]) == exp_rows, f"system {s}: incremental pivot rows differ"
+        assert list(out["pcol"][s][:p]) == exp_cols, f"system {s}: incremental pivot cols differ"
+        _check_system(code, masks[s], d[s], r[s], None if flip is None else flip[s], out, s, tol_dy=1e-8,
+                      check_pivots=False)
+    return out
+
+
+def test_incremental_mts_matches_oracle_alg6():
+    """SURVEY f-1: Alg. 6 with the Triangulation Step bit-exact vs the oracle on
+    config-1 systems with partial rows and flips, and on all-equal weights (tie rules)."""
+    code = config_code(1)
+    S = 16
+    sy = c5_systems(range(S), code, lo=-3, hi=3, present_frac=0.7)
+    flip = np.random.default_rng(12).integers(0, 2, size=(S, code.n)).astype(np.uint8)
+    _check_incremental(code, sy.masks, sy.d, sy.r, flip)
+    _check_incremental(code, sy.masks[:6], np.ones_like(sy.d[:6]), sy.r[:6], flip[:6])
+
+
 def test_thm5_rowwise_contains_basic_columns_near_integral_optimum():
     """Thm 5: near the optimum of an LP with an integral solution, the row-wise MTS
     contains every basic column.  Late-IPM weights are formed from the oracle's LP optimum x*

@@ -1,6 +1,6 @@
 # final-build captures: C2 3.0 dB decode (launch list + full), C2 2.0 dB decode (full), C5 step kernel (full)
 mkdir -p gpurun_out
-TAG=r2d
+TAG=${TAG:-r2d}
 CMD="python bench.py --frames 1184 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --snr-sweep 0 --step-systems 0"
 CMD2="python bench.py --frames 592 --snr-idx 0 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --snr-sweep 0 --step-systems 0"
 CMD5="python bench.py --frames 148 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --snr-sweep 0 --step-systems 16384"
