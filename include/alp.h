@@ -217,8 +217,8 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
                         int32_t* pivot_rows, int32_t* pivot_cols, void* workspace,
                         size_t workspace_bytes, const alp_params* params, void* stream);
 
-/* Diagnostics: when `records` (DEVICE, capacity x 104-byte records {int32 frame, lp, ipm_it,
- * p, status, pcg_iters; fp64 true relres, recursive relres, d2_min, d2_max, mu, ||r_b||inf,
+/* Diagnostics: when `records` (DEVICE, capacity x 112-byte records {int32 frame, lp, ipm_it,
+ * p, status, pcg_iters, back-sweep levels, forward-sweep levels; fp64 true relres, recursive relres, d2_min, d2_max, mu, ||r_b||inf,
  * ||r_c||inf, gap, beta_P, beta_D}) is non-NULL, every subsequent
  * alp_decode appends one record per Newton-step solve (order unspecified, records beyond
  * capacity dropped).  NULL disables.  Process-wide; not thread safe; not for production. */

@@ -19,7 +19,7 @@ namespace alp {
 
 // Optional per-Newton-step trace (alp_debug_trace): one record per step solve.
 struct TraceRec {
-  int frame, lp, ipm_it, p, status, iters;
+  int frame, lp, ipm_it, p, status, iters, nLb, nLf;
   double relres, rec_relres, d2min, d2max, mu, rb, rc, gap, beta_p, beta_d;
 };
 __device__ TraceRec* g_trace = nullptr;

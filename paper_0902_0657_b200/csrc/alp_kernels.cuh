@@ -357,7 +357,7 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
       if (lane == 0) {
         int slot = atomicAdd(&g_trace_n, 1);
         if (slot < g_trace_cap)
-          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, pr.relres, pr.rec_relres, dmn, dmx, mu, rbn, rcn, gap, bP, bD};
+          g_trace[slot] = TraceRec{(int)frame_id, lp_id, it, p, pr.status, pr.iters, nLb, nLf, pr.relres, pr.rec_relres, dmn, dmx, mu, rbn, rcn, gap, bP, bD};
       }
     }
     bool bad = false;
@@ -402,6 +402,23 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
   return out;
 }
 
+
+#ifdef ALP_POISON
+// Diagnostics build (-DALP_POISON): before each frame / system, fill the warp's shared window
+// and its whole global slot with NaN bit patterns, so any read of state that the frame did not
+// write first changes the outputs (tools/poison_check.py compares against the normal build;
+// stands in for compute-sanitizer initcheck, which this pool does not allow).
+__device__ __forceinline__ void poison_frame(const Frame& F, char* slot) {
+  const Layout& L = *F.L;
+  unsigned long long* s8 = reinterpret_cast<unsigned long long*>(slot);
+  for (long long k = F.lane; k < L.slot_bytes / 8; k += 32) s8[k] = 0xfff8dead0000beefull;
+  if (!L.win_global) {
+    unsigned long long* w8 = reinterpret_cast<unsigned long long*>(F.sm);
+    for (int k = F.lane; k < L.smem_bytes / 8; k += 32) w8[k] = 0xfff8dead0000beefull;
+  }
+  __syncwarp();
+}
+#endif
 
 // MALP-A / MALP-B decode of one frame (Alg. 3; outputs P:143, C-11..C-15).
 __device__ void decode_frame(Frame& F, const Params& P, const double* g, long long f,
@@ -574,6 +591,9 @@ __global__ void __launch_bounds__(256, ALP_MINB) alp_decode_kernel(DCode C, Para
     if (lane == 0) f = (long long)atomicAdd(counter, 1ull);   // 64-bit: no wrap at any n_frames
     f = __shfl_sync(FULL, f, 0);
     if (f >= n_frames) break;
+#ifdef ALP_POISON
+    poison_frame(F, slot);
+#endif
     decode_frame(F, P, llr + f * C.n, f, O);
   }
 }
@@ -602,6 +622,9 @@ __global__ void __launch_bounds__(256, 1) pcg_step_kernel(DCode C, Params P, Lay
     if (lane == 0) s = (long long)atomicAdd(counter, 1ull);
     s = __shfl_sync(FULL, s, 0);
     if (s >= n_sys) break;
+#ifdef ALP_POISON
+    poison_frame(F, slot);
+#endif
     for (int j = lane; j < m; j += 32) F.mask[j] = io.masks[s * m + j];
     for (int i = lane; i < n; i += 32) F.flip[i] = io.flip ? (io.flip[s * n + i] ? 1 : 0) : 0;
     __syncwarp();

@@ -14,7 +14,7 @@ import paper_0902_0657_b200 as alp
 from synth import config_code, config_frames
 
 REC = np.dtype([("frame", "<i4"), ("lp", "<i4"), ("it", "<i4"), ("p", "<i4"), ("status", "<i4"),
-                ("iters", "<i4"), ("relres", "<f8"), ("rec", "<f8"), ("d2min", "<f8"), ("d2max", "<f8"),
+                ("iters", "<i4"), ("nLb", "<i4"), ("nLf", "<i4"), ("relres", "<f8"), ("rec", "<f8"), ("d2min", "<f8"), ("d2max", "<f8"),
                 ("mu", "<f8"), ("rb", "<f8"), ("rc", "<f8"), ("gap", "<f8"), ("bP", "<f8"), ("bD", "<f8")])
 snr = int(os.environ.get("SNR", "0"))
 F = int(os.environ.get("NF", "256"))

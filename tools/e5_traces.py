@@ -8,8 +8,9 @@ to capture the Newton systems at IPM iterations 8 and 18; each system is then so
 ipm_step_pcg with the column-wise MTS preconditioner (precond=0, Alg. 7), the row-wise MTS with
 diagonal expansion (precond=2, Alg. 8) and plain CG (precond=1), capped at k = 1..K iterations,
 giving the TRUE relative residual ||w - Q dy||/||w|| after k iterations (the paper plots the
-squared ratio, G15).  Output: gpurun_out/e5_traces.json.  The incremental MTS curve (Alg. 6,
-O(q^2)) is not reproduced on the GPU (oracle only).
+squared ratio, G15).  The incremental MTS (precond=3, Alg. 6 with the Triangulation Step; O(q)
+triangulations per build) is traced on the coarse grid k = 10, 20, ..., K.  Output:
+gpurun_out/e5_traces.json.
 """
 import json
 import os
@@ -72,9 +73,9 @@ for label, snr in (("integral_1.5dB", 1.5), ("fractional_1.0dB", 1.0)):
         td = torch.from_numpy(d).cuda()
         tr = torch.from_numpy(r).cuda()
         curves = {}
-        for name, pc in (("column-wise MTS", 0), ("row-wise MTS", 2), ("CG", 1)):
+        for name, pc in (("column-wise MTS", 0), ("row-wise MTS", 2), ("CG", 1), ("incremental MTS", 3)):
             res = []
-            for k in range(1, K + 1):
+            for k in (range(1, K + 1) if pc != 3 else range(10, K + 1, 10)):
                 prm = alp.default_params(precond=pc, pcg_max_iter=k, pcg_rel_tol=1e-14)
                 sol = alp.ipm_step_pcg(c, tm, td, tr, params=prm)
                 torch.cuda.synchronize()
@@ -86,6 +87,7 @@ for label, snr in (("integral_1.5dB", 1.5), ("fractional_1.0dB", 1.0)):
             "p": p, "q": n + p, "kappa_Q": float(ev[-1] / max(ev[0], 1e-300)),
             "true_relres_after_k": curves}
         print(label, "frame", f, "it", it, "p", p, "kappa %.2e" % (ev[-1] / max(ev[0], 1e-300)),
-              {k: ["%.1e" % v for v in vals[9::10]] for k, vals in curves.items()}, flush=True)
+              {k: ["%.1e" % v for v in (vals[9::10] if len(vals) == K else vals)] for k, vals in curves.items()},
+              flush=True)
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/e5_traces.json", "w"), indent=1)
