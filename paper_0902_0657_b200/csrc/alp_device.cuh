@@ -1339,29 +1339,65 @@ struct OffReg {
 // pivot column, stored at index R.  A record is RBW uint4 (8 u16 each): [R | neg, dep...]; the
 // records of a level are contiguous, and each level's first 32-slot chunk is prefetched during
 // the previous level (records do not depend on the values being computed).
-template <int RBW>
+// The <= ND dependency gathers of a step are predicated loads issued back to back (no load
+// inside the sum chain), and the signed terms are summed as a balanced tree: the step's latency
+// is one gather round plus log2(ND + 1) fp64 adds (measured: with a load per dependency inside the sum chain, a level cost ~700
+// cycles on the late-IPM systems of fractional frames, tools/straggler_trace.py).
+template <int RBW, int ND>
 __device__ __forceinline__ void back_step(const uint4 (&q)[RBW], const double* rS, double* fS) {
   const uint16_t* v = reinterpret_cast<const uint16_t*>(&q[0]);
   const int head = v[0];
   const int R = head & 0x7fff;
-  double acc = rS[R];
+  if constexpr (ND > 7) {   // d_c > 8 (config 3): the serial chain (the tree's registers would
+    double acc = rS[R];     // spill across the whole inlined kernel)
 #pragma unroll
-  for (int d = 1; d < 8 * RBW; ++d) {
-    const int dep = v[d];
-    if (dep != (int)NODEP) {
-      const double fv = fS[dep & 0x7fff];
-      acc = (dep & 0x8000) ? acc + fv : acc - fv;
+    for (int d = 1; d <= ND; ++d) {
+      const int dep = v[d];
+      if (dep != (int)NODEP) {
+        const double fv = fS[dep & 0x7fff];
+        acc = (dep & 0x8000) ? acc + fv : acc - fv;
+      }
     }
+    fS[R] = (head & 0x8000) ? -acc : acc;
+  } else {
+  double t[ND + 1];
+  t[0] = rS[R];
+#pragma unroll
+  for (int d = 1; d <= ND; ++d) {
+    const int dep = v[d];
+    const double fv = (dep != (int)NODEP) ? fS[dep & 0x7fff] : 0.0;   // predicated gather
+    t[d] = (dep & 0x8000) ? fv : -fv;
   }
-  fS[R] = (head & 0x8000) ? -acc : acc;
+#pragma unroll
+  for (int w = 1; w <= ND; w *= 2)
+#pragma unroll
+    for (int d = 0; d + w <= ND; d += 2 * w) t[d] += t[d + w];
+  fS[R] = (head & 0x8000) ? -t[0] : t[0];
+  }
 }
 
-template <int RBW>
+template <int RBW, int ND>
 __device__ __forceinline__ void back_sweep_t(const Frame& F, int nLb, const double* rS, double* fS) {
   const uint4* rec = reinterpret_cast<const uint4*>(F.recB_());
   OffReg off;
   off.load(F.offB_(), nLb, F.lane);
   int a = off(0), b = off(1);
+  if constexpr (RBW > 1) {
+    // d_c > 7 (config 3): no prefetch (two live 32-byte records would raise the register
+    // allocation of the whole inlined decode kernel; measured ~200 B of spills)
+    for (int lvl = 0; lvl < nLb; ++lvl) {
+      for (int s = a + F.lane; s < b; s += 32) {
+        uint4 t[RBW];
+#pragma unroll
+        for (int k = 0; k < RBW; ++k) t[k] = rec[(size_t)s * RBW + k];
+        back_step<RBW, ND>(t, rS, fS);
+      }
+      __syncwarp();
+      a = b;
+      b = (lvl + 2 <= nLb) ? off(lvl + 2) : b;
+    }
+    return;
+  }
   uint4 cur[RBW];
   bool hc = a + F.lane < b;
   if (hc) {
@@ -1376,12 +1412,12 @@ __device__ __forceinline__ void back_sweep_t(const Frame& F, int nLb, const doub
 #pragma unroll
       for (int k = 0; k < RBW; ++k) nxt[k] = rec[(size_t)(b + F.lane) * RBW + k];
     }
-    if (hc) back_step<RBW>(cur, rS, fS);
+    if (hc) back_step<RBW, ND>(cur, rS, fS);
     for (int s = a + F.lane + 32; s < b; s += 32) {
       uint4 t[RBW];
 #pragma unroll
       for (int k = 0; k < RBW; ++k) t[k] = rec[(size_t)s * RBW + k];
-      back_step<RBW>(t, rS, fS);
+      back_step<RBW, ND>(t, rS, fS);
     }
     __syncwarp();
     a = b;
@@ -1394,8 +1430,10 @@ __device__ __forceinline__ void back_sweep_t(const Frame& F, int nLb, const doub
 
 __device__ ALP_PCGPART void back_sweep(const Frame& F, int nLb, const double* rS, double* fS) {
   if (nLb <= 0) return;
-  if (F.C->RB == 8) back_sweep_t<1>(F, nLb, rS, fS);
-  else back_sweep_t<2>(F, nLb, rS, fS);
+  // dependency slots per record: position t in N(R) (t < d_c; the pivot's own column is NODEP)
+  if (F.C->dcr <= 6) back_sweep_t<1, 6>(F, nLb, rS, fS);
+  else if (F.C->RB == 8) back_sweep_t<1, 7>(F, nLb, rS, fS);
+  else back_sweep_t<2, 15>(F, nLb, rS, fS);
 }
 
 // Forward substitution A_M^T z = D_M^-2 f (P:585 stages 2-3), z overwriting f in place (row R's
@@ -1404,21 +1442,17 @@ __device__ ALP_PCGPART void back_sweep(const Frame& F, int nLb, const double* rS
 __device__ __forceinline__ double fwd_step(uint2 rec, double dinv, double* zS) {
   const int head = rec.x & 0xffff;
   const int R = head & 0x7fff;
-  const double fr = zS[R];
-  double acc = fr * dinv;
   const int d1 = rec.x >> 16, d2 = rec.y & 0xffff, d3 = rec.y >> 16;
-  if (d1 != (int)NODEP) {
-    const double zv = zS[d1 & 0x7fff];
-    acc = (d1 & 0x8000) ? acc + zv : acc - zv;
-  }
-  if (d2 != (int)NODEP) {
-    const double zv = zS[d2 & 0x7fff];
-    acc = (d2 & 0x8000) ? acc + zv : acc - zv;
-  }
-  if (d3 != (int)NODEP) {
-    const double zv = zS[d3 & 0x7fff];
-    acc = (d3 & 0x8000) ? acc + zv : acc - zv;
-  }
+  const bool u1 = d1 != (int)NODEP, u2 = d2 != (int)NODEP, u3 = d3 != (int)NODEP;
+  // predicated gathers issued together, then a two-level add tree
+  const double fr = zS[R];
+  const double z1 = u1 ? zS[d1 & 0x7fff] : 0.0;   // predicated gathers
+  const double z2 = u2 ? zS[d2 & 0x7fff] : 0.0;
+  const double z3 = u3 ? zS[d3 & 0x7fff] : 0.0;
+  const double t1 = (d1 & 0x8000) ? z1 : -z1;
+  const double t2 = (d2 & 0x8000) ? z2 : -z2;
+  const double t3 = (d3 & 0x8000) ? z3 : -z3;
+  const double acc = (fr * dinv + t1) + (t2 + t3);
   zS[R] = (head & 0x8000) ? -acc : acc;
   return fr * fr * dinv;
 }
@@ -1536,20 +1570,20 @@ __device__ ALP_PCGPART double spmv_vars(const Frame& F, const DCode& C) {
       dv[u] = ok ? d2[i] : 0.0;
       // scalar u16 index loads (measured: 16-byte vector loads of the padded rows were 1.8x slower)
 #pragma unroll
-      for (int kk = 0; kk < DVMAX; ++kk) jn[u][kk] = ((sv[u] >> kk) & 1) ? (int)var_chk[i * DVMAX + kk] : -1;
+      for (int kk = 0; kk < DVMAX; ++kk) jn[u][kk] = ((sv[u] >> kk) & 1) ? (int)var_chk[i * DVMAX + kk] : 0;
     }
+    // predicated gathers, summed as a tree
     double acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      acc[u] = 0.0;
+      double g[DVMAX];
 #pragma unroll
       for (int kk = 0; kk < DVMAX; ++kk) {
-        if (jn[u][kk] >= 0) {
-          double hv = hS[jn[u][kk]];
-          if (ABS) acc[u] += fabs(hv);
-          else acc[u] = ((sv[u] >> (4 + kk)) & 1) ? acc[u] - hv : acc[u] + hv;
-        }
+        const bool use = (sv[u] >> kk) & 1;
+        const double hv = use ? hS[jn[u][kk]] : 0.0;   // predicated gather: absent rows load nothing
+        g[kk] = ABS ? fabs(hv) : (((sv[u] >> (4 + kk)) & 1) ? -hv : hv);
       }
+      acc[u] = (g[0] + g[1]) + (g[2] + g[3]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1616,19 +1650,24 @@ __device__ ALP_PCGPART double spmv_checks(const Frame& F, const DCode& C, double
         rj[u] = W[jj];
       }
 #pragma unroll
-      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg) ? (int)chk_var[j * dc + t] : -1;
+      for (int t = 0; t < DCT; ++t) in[u][t] = (t < deg && (sc[u] & PRESENT)) ? (int)chk_var[j * dc + t] : -1;
     }
 #pragma unroll
     for (int u = 0; u < UC; ++u) {
-      double l = d2s[u] * ((MODE == CP_ABS) ? fabs(hj[u]) : hj[u]);
+      // predicated gathers (absent rows and slots past the degree load nothing), summed as a tree
+      double g[DCT + 1];
+      g[0] = d2s[u] * ((MODE == CP_ABS) ? fabs(hj[u]) : hj[u]);
 #pragma unroll
       for (int t = 0; t < DCT; ++t) {
-        if (in[u][t] >= 0) {
-          const double tv = tS[in[u][t]];
-          if (MODE == CP_ABS) l += tv;
-          else l = ((sc[u] >> t) & 1) ? l - tv : l + tv;
-        }
+        const bool use = in[u][t] >= 0;
+        const double tv = use ? tS[in[u][t]] : 0.0;
+        g[t + 1] = (MODE == CP_ABS) ? tv : (((sc[u] >> t) & 1) ? -tv : tv);
       }
+#pragma unroll
+      for (int w = 1; w <= DCT; w *= 2)
+#pragma unroll
+        for (int d = 0; d + w <= DCT; d += 2 * w) g[d] += g[d + w];
+      const double l = g[0];
       const int j = j0 + 32 * u;
       if (!(sc[u] & PRESENT)) continue;   // also j >= m (sc = 0)
       if (MODE == CP_UPDATE) {

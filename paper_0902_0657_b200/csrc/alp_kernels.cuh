@@ -3,7 +3,10 @@
 namespace alp {
 namespace ALP_NS {
 
-constexpr int UB = 4;   // IPM-body elements per lane per step (load batching)
+#ifndef ALP_UB
+#define ALP_UB 4
+#endif
+constexpr int UB = ALP_UB;   // IPM-body elements per lane per step (load batching)
 
 struct IpmOut {
   int iters, status, pcg_iters, solves, p4_fail, true_fail;
