@@ -495,6 +495,7 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
   uint16_t* cd = cB;
   for (int sh = 0; sh < 32; sh += 4) {
     unsigned long long q0 = 0ull, q1 = 0ull, q2 = 0ull, q3 = 0ull;
+#pragma unroll 4
     for (int i = lo; i < hi; ++i) {
       const int dg = (ks[i] >> sh) & 0xf;
       const unsigned long long inc = 1ull << (16 * (dg & 3));
@@ -528,13 +529,33 @@ __device__ ALP_HEAVY int sort_columns(const Frame& F) {
       continue;
     }
     __syncwarp();
+    // this lane's 16 running digit offsets packed two per register (u16: Q <= 65535), so the
+    // scatter has no read-after-write chain through shared memory
+    // (eight named registers with select chains: an indexed array would go to local memory)
+#define ALP_OFF2(w) (offs[(2 * (w)) * 32 + F.lane] | (offs[(2 * (w) + 1) * 32 + F.lane] << 16))
+    uint32_t o0 = ALP_OFF2(0), o1 = ALP_OFF2(1), o2 = ALP_OFF2(2), o3 = ALP_OFF2(3), o4 = ALP_OFF2(4),
+             o5 = ALP_OFF2(5), o6 = ALP_OFF2(6), o7 = ALP_OFF2(7);
+#undef ALP_OFF2
+#pragma unroll 2
     for (int i = lo; i < hi; ++i) {
       const uint32_t k = ks[i];
+      const uint16_t cv = cs[i];
       const int dg = (k >> sh) & 0xf;
-      const uint32_t at = offs[dg * 32 + F.lane];
-      offs[dg * 32 + F.lane] = at + 1u;
+      const int w = dg >> 1, hs = 16 * (dg & 1);
+      const uint32_t lo4 = (w & 2) ? ((w & 1) ? o3 : o2) : ((w & 1) ? o1 : o0);
+      const uint32_t hi4 = (w & 2) ? ((w & 1) ? o7 : o6) : ((w & 1) ? o5 : o4);
+      const uint32_t at = (((w & 4) ? hi4 : lo4) >> hs) & 0xffffu;
+      const uint32_t inc = 1u << hs;
+      o0 += (w == 0) ? inc : 0u;
+      o1 += (w == 1) ? inc : 0u;
+      o2 += (w == 2) ? inc : 0u;
+      o3 += (w == 3) ? inc : 0u;
+      o4 += (w == 4) ? inc : 0u;
+      o5 += (w == 5) ? inc : 0u;
+      o6 += (w == 6) ? inc : 0u;
+      o7 += (w == 7) ? inc : 0u;
       kd[at] = k;
-      cd[at] = cs[i];
+      cd[at] = cv;
     }
     __syncwarp();
     uint32_t* tk = ks; ks = kd; kd = tk;
@@ -1551,6 +1572,11 @@ __device__ ALP_PCGPART double spmv_vars(const Frame& F, const DCode& C) {
   // step k covers variables 32 U k + lane + 32 u and, for the slack columns, check 32 k + lane
   // (d2_{n+j} h_j^2), so both sums take one loop (m <= U n for every code in use; a remainder
   // loop covers the rest)
+  // d^2 lives in the slot (L2): each step's weights are loaded one step ahead
+  double dnx[U], dsnx = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) dnx[u] = (F.lane + 32 * u < n) ? d2[F.lane + 32 * u] : 0.0;
+  if (!ABS && F.lane < m) dsnx = d2s[F.lane];
   int k = 0;
   for (int i0 = F.lane; i0 < n; i0 += 32 * U, ++k) {
     uint8_t sv[U];
@@ -1560,14 +1586,17 @@ __device__ ALP_PCGPART double spmv_vars(const Frame& F, const DCode& C) {
     double hs = 0.0, ds = 0.0;
     if (!ABS && js < m && (sgnC[js] & PRESENT)) {   // (absent rows: d2 is stale slot memory)
       hs = hS[js];
-      ds = d2s[js];
+      ds = dsnx;
     }
+    if (!ABS && js + 32 < m) dsnx = d2s[js + 32];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + 32 * u;
       const bool ok = i < n;
       sv[u] = ok ? sgnV[i] : (uint8_t)0;
-      dv[u] = ok ? d2[i] : 0.0;
+      dv[u] = dnx[u];
+      const int inx = i + 32 * U;
+      dnx[u] = (inx < n) ? d2[inx] : 0.0;
       // scalar u16 index loads (measured: 16-byte vector loads of the padded rows were 1.8x slower)
 #pragma unroll
       for (int kk = 0; kk < DVMAX; ++kk) jn[u][kk] = ((sv[u] >> kk) & 1) ? (int)var_chk[i * DVMAX + kk] : 0;
@@ -1630,6 +1659,10 @@ __device__ ALP_PCGPART double spmv_checks(const Frame& F, const DCode& C, double
 #endif
   constexpr int UC = ALP_SPMV_UC;   // checks per lane per step
   double acc2 = 0.0;
+  // the slack weights d2_{n+j} (slot, L2) are loaded one step ahead
+  double dnx[UC];
+#pragma unroll
+  for (int u = 0; u < UC; ++u) dnx[u] = d2s_[min(F.lane + 32 * u, m - 1)];
   for (int j0 = F.lane; j0 < m; j0 += 32 * UC) {
     uint16_t sc[UC];
     double hj[UC], d2s[UC], rj[UC], yj[UC];
@@ -1642,7 +1675,8 @@ __device__ ALP_PCGPART double spmv_checks(const Frame& F, const DCode& C, double
       sc[u] = ok ? sgnC[j] : (uint16_t)0;
       const int deg = ok ? (int)chk_deg[j] : 0;
       hj[u] = hS[jj];
-      d2s[u] = d2s_[jj];
+      d2s[u] = dnx[u];
+      dnx[u] = d2s_[min(j + 32 * UC, m - 1)];
       if (MODE == CP_UPDATE) {
         rj[u] = rS[jj];
         yj[u] = dyS[jj];
@@ -1792,7 +1826,8 @@ __device__ ALP_CALL_PCG PcgResult pcg_solve(const Frame& F, const Params& P, int
   double* dyS = F.dy_();
   const uint16_t* __restrict__ sgnC = F.sgnC_();
   double ww = 0.0;
-  for (int j = F.lane; j < C.m; j += 32) {
+#pragma unroll 4
+  for (int j = F.lane; j < C.m; j += 32) {   // (unrolled: the w loads from the slot overlap)
     const bool pr = (sgnC[j] & PRESENT) != 0;
     const double wj = pr ? F.w[j] : 0.0;
     ww += wj * wj;

@@ -90,6 +90,41 @@ __device__ __forceinline__ void ipm_rows_w(const DCode& C, int lane, const uint1
   }
 }
 
+// rho = r_b - A dx on the present rows (the step residual moved onto the basis, C-32), UBR rows
+// per lane per step with every gather issued before the sums (the slot arrays are L2-resident).
+template <int DCT>
+__device__ __forceinline__ void ipm_rows_rho(const DCode& C, int lane, const uint16_t* __restrict__ SC,
+                                             const double* __restrict__ RBv, const double* __restrict__ V,
+                                             double* __restrict__ rS) {
+  constexpr int UBR = (DCT <= 6) ? UB : 1;
+  const int n = C.n, m = C.m;
+  for (int j0 = lane; j0 < m; j0 += 32 * UBR) {
+    double vs[UBR][DCT], rb[UBR], vsl[UBR];
+    uint16_t sc[UBR];
+#pragma unroll
+    for (int u = 0; u < UBR; ++u) {
+      const int j = min(j0 + 32 * u, m - 1);
+      sc[u] = (j0 + 32 * u < m) ? SC[j] : (uint16_t)0;
+      const int deg = (sc[u] & PRESENT) ? (int)C.chk_deg[j] : 0;
+      rb[u] = RBv[j];
+      vsl[u] = V[n + j];
+#pragma unroll
+      for (int t = 0; t < DCT; ++t) vs[u][t] = (t < deg) ? V[C.chk_var[j * C.dc + t]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UBR; ++u) {
+      if (j0 + 32 * u >= m) continue;
+      double acc = 0.0;
+      if (sc[u] & PRESENT) {
+        acc = rb[u] - vsl[u];
+#pragma unroll
+        for (int t = 0; t < DCT; ++t) acc = ((sc[u] >> t) & 1) ? acc + vs[u][t] : acc - vs[u][t];
+      }
+      rS[j0 + 32 * u] = acc;
+    }
+  }
+}
+
 // =====================================================================================
 // Infeasible primal-dual path-following IPM (§IV-B) on the current pool LP
 // min c^T x, A x = b, x >= 0 (q = n + p columns; absent slack columns excluded).
@@ -307,27 +342,22 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
     if (P.basis_correction && nLb > 0) {
       double* rS = F.r_();
       double* fS = F.fz_();
-      for (int j = lane; j < m; j += 32) {
-        uint16_t s = SC[j];
-        double rho = 0.0;
-        if (s & PRESENT) {
-          int deg = C.chk_deg[j];
-          double acc = RBv[j] - V[n + j];
-          for (int t = 0; t < deg; ++t) {
-            double xi = V[chk_nb(C, j, t)];
-            acc = ((s >> t) & 1) ? acc + xi : acc - xi;
-          }
-          rho = acc;
-        }
-        rS[j] = rho;
-      }
+      if (C.dcr <= 6) ipm_rows_rho<6>(C, lane, SC, RBv, V, rS);
+      else ipm_rows_rho<DCMAX>(C, lane, SC, RBv, V, rS);
       __syncwarp();
       back_sweep(F, nLb, rS, fS);   // f = A_M^-1 rho, f_R = component of row R's pivot column
       __syncwarp();
       const uint16_t* pcolR = F.pcolR_();
-      for (int j = lane; j < m; j += 32) {
-        const uint16_t c = pcolR[j];
-        if (c != NONE16) V[c] += fS[j];
+      for (int j0 = lane; j0 < m; j0 += 32 * UB) {   // dx_M += f (distinct pivot columns)
+        uint16_t cs[UB];
+        double vc[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) cs[u] = (j0 + 32 * u < m) ? pcolR[j0 + 32 * u] : NONE16;
+#pragma unroll
+        for (int u = 0; u < UB; ++u) vc[u] = (cs[u] != NONE16) ? V[cs[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < UB; ++u)
+          if (cs[u] != NONE16) V[cs[u]] = vc[u] + fS[j0 + 32 * u];
       }
       __syncwarp();
     }
@@ -387,11 +417,22 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
         bad |= !isfinite(xn) || !isfinite(zn);
       }
     }
-    for (int j = lane; j < m; j += 32) {
-      if (!(SC[j] & PRESENT)) continue;
-      double yn = Y[j] + bD * DY[j];
-      Y[j] = yn;
-      bad |= !isfinite(yn);
+    for (int j0 = lane; j0 < m; j0 += 32 * UB) {
+      double yv[UB];
+      bool ok[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int j = j0 + 32 * u;
+        ok[u] = (j < m) && (SC[min(j, m - 1)] & PRESENT);
+        yv[u] = ok[u] ? Y[j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (!ok[u]) continue;
+        const double yn = yv[u] + bD * DY[j0 + 32 * u];
+        Y[j0 + 32 * u] = yn;
+        bad |= !isfinite(yn);
+      }
     }
     __syncwarp();
     ++it;
@@ -498,6 +539,7 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
     true_fail += o.true_fail;
     max_rec = fmax(max_rec, o.max_rec);
     max_true = fmax(max_true, o.max_true);
+#pragma unroll 4
     for (int i = lane; i < n; i += 32) {
       double xi = F.x[i];
       F.u[i] = F.flip[i] ? 1.0 - xi : xi;
