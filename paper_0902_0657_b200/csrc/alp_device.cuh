@@ -676,6 +676,133 @@ __device__ __forceinline__ void peel_picks_reg(const Frame& F, int p, const uint
   }
 }
 
+// Batched variant of the same picks (-DALP_PEEL_BATCH; measured no faster).  A batch
+// takes the first NB = 32 / RS set bits of DEG1, ranks r_0 < r_1 < ... with live rows R_g, and
+// makes all picks of its longest prefix that the sequential loop above would make in the same
+// order: candidate i is pick k + i when
+//   (a) R_i differs from R_0..R_{i-1} (else the earlier kill empties r_i's column), and
+//   (b) every column that the kills of R_0..R_{i-1} can bring to degree 1 ranks after r_i.
+// For (b) the "threat" of row R_g is the lowest rank among its columns other than r_g with >= 2
+// live rows (the only columns a kill can move into DEG1; a degree-1 column of R_g other than
+// r_g ranked before r_i would itself be a candidate with row R_g and fail (a)).  By induction
+// the sequential loop then finds r_i at the head of DEG1 after the first i picks.  The kills
+// of a batch commute (live-row count decrement, XOR of the row id), so lane (g, t) applies row
+// R_g's column t with shared-memory atomics on the containing 32-bit words, and the DEG1 bits
+// (Refinement of (b): a column with c >= 3 live rows is a threat only if >= c - 1 of the NB
+// candidate rows hold it — the prefix's kills are a subset of the candidates'.)
+// follow the final counts.  Lane layout: g = lane / RS (candidate), t = lane % RS (column).
+template <int K, int RS>
+__device__ __forceinline__ void peel_picks_batch(const Frame& F, int p, const uint16_t* __restrict__ order,
+                                                 const uint16_t* __restrict__ rrank,
+                                                 uint8_t* cntR, uint16_t* xrR,
+                                                 unsigned long long* bm, uint16_t* pos,
+                                                 uint16_t* pcol, uint16_t* prow) {
+  constexpr int NB = 32 / RS;
+  constexpr int BIG = 0x7fffffff;
+  const int W = F.C->W;
+  const int g = F.lane / RS, t = F.lane % RS;
+  unsigned long long wd[K > 0 ? K : 1];
+#pragma unroll
+  for (int kk = 0; kk < K; ++kk) {
+    const int w = 32 * kk + F.lane;
+    wd[kk] = (w < W) ? bm[w] : 0ull;
+  }
+  for (int k = 0; k < p;) {
+    // the first NB set bits of DEG1 in rank order (warp-uniform)
+    int cand[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) cand[i] = BIG;
+    int nc = 0;
+    // K > 0: lane l holds words l, 32 + l, ... in registers; K == 0 (large codes): scan the
+    // shared bitmap 32 words at a time
+    for (int kk = 0; ((K > 0) ? (kk < K) : (32 * kk < W)) && nc < NB; ++kk) {
+      unsigned long long wk = 0ull;
+      if constexpr (K > 0) {
+#pragma unroll
+        for (int q = 0; q < (K > 0 ? K : 1); ++q) wk = (q == kk) ? wd[q] : wk;
+      } else {
+        const int w = 32 * kk + F.lane;
+        wk = (w < W) ? bm[w] : 0ull;
+      }
+      unsigned bal = __ballot_sync(FULL, wk != 0ull);
+      while (bal != 0u && nc < NB) {
+        const int src = __ffs(bal) - 1;
+        unsigned long long w0 = __shfl_sync(FULL, wk, src);
+        while (w0 != 0ull && nc < NB) {
+          const int r = (32 * kk + src) * 64 + (__ffsll((long long)w0) - 1);
+#pragma unroll
+          for (int i = 0; i < NB; ++i) cand[i] = (i == nc) ? r : cand[i];
+          ++nc;
+          w0 &= w0 - 1ull;
+        }
+        bal &= bal - 1u;
+      }
+    }
+    int rg = cand[0];
+#pragma unroll
+    for (int i = 1; i < NB; ++i) rg = (g == i) ? cand[i] : rg;
+    const bool vg = g < nc;
+    const int Rg = vg ? (int)xrR[rg] : -1;
+    const int x = vg ? (int)rrank[Rg * RS + t] : (int)NONE16;
+    const bool xv = x != (int)NONE16;
+    const int c = xv ? (int)cntR[x] : 0;
+    // a column with c live rows reaches degree 1 only if >= c - 1 of the candidate rows hold it
+    const unsigned same = __match_any_sync(FULL, xv ? (unsigned)x : 0x10000u + (unsigned)F.lane);
+    int thr = (xv && x != rg && c >= 2 && c - __popc(same) <= 1) ? x : BIG;
+#pragma unroll
+    for (int o = 1; o < RS; o <<= 1) thr = min(thr, __shfl_xor_sync(FULL, thr, o));
+    int Rs[NB], Th[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      Rs[i] = __shfl_sync(FULL, Rg, i * RS);
+      Th[i] = __shfl_sync(FULL, thr, i * RS);
+    }
+    // longest valid prefix (warp-uniform)
+    int nb = 1, tmin = Th[0];
+#pragma unroll
+    for (int i = 1; i < NB; ++i) {
+      bool ok = (nb == i) && (i < nc) && (k + i < p) && (tmin > cand[i]);
+#pragma unroll
+      for (int j = 0; j < i; ++j) ok = ok && (Rs[j] != Rs[i]);
+      if (ok) {
+        nb = i + 1;
+        tmin = min(tmin, Th[i]);
+      }
+    }
+    // kill R_0..R_{nb-1}: count and XOR updates commute -> atomics on the containing words
+    const bool act = (g < nb) && xv;
+    const unsigned accm = __ballot_sync(FULL, act);
+    if (act) {
+      const uintptr_t ac = (uintptr_t)(cntR + x), ax = (uintptr_t)(xrR + x);
+      atomicSub(reinterpret_cast<unsigned*>(ac & ~(uintptr_t)3), 1u << (8 * (ac & 3)));
+      atomicXor(reinterpret_cast<unsigned*>(ax & ~(uintptr_t)3), (unsigned)Rg << (8 * (ax & 2)));
+      // DEG1 bit from the final count c - (accepted rows holding x): the same idempotent
+      // update from every lane that shares x
+      const int fc = c - __popc(same & accm);
+      if (fc == 1) atomicOr(&bm[x >> 6], 1ull << (x & 63));
+      else if (fc == 0) atomicAnd(&bm[x >> 6], ~(1ull << (x & 63)));
+    }
+    if (t == 0 && g < nb) {
+      pos[Rg] = (uint16_t)(k + g);
+      pcol[Rg] = order[rg];
+      prow[k + g] = (uint16_t)Rg;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const int w = 32 * kk + F.lane;
+      wd[kk] = (w < W) ? bm[w] : 0ull;
+    }
+    k += nb;
+#ifdef ALP_PEEL_COUNT
+    if (F.lane == 0) {   // diagnostics: batches in the sort clock, picks in the peel clock
+      F.cyc[CY_SORT] += 1;
+      F.cyc[CY_PEEL] += nb;
+    }
+#endif
+  }
+}
+
 // Shared-memory bitmap variant for large codes (W > 128 words).
 __device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16_t* order,
                                              const uint16_t* rrank, int RS, uint8_t* cntR,
@@ -718,6 +845,9 @@ __device__ __noinline__ void peel_picks_smem(const Frame& F, int p, const uint16
 __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const Layout& L = *F.L;
+#ifdef ALP_PEEL_SPLIT
+  const long long tp0 = clock64();
+#endif
   const uint16_t* order = F.S<uint16_t>(L.s_order);
   uint16_t* rank = F.S<uint16_t>(L.s_rank);
   uint8_t* cntR = F.S<uint8_t>(L.s_cnt);
@@ -763,11 +893,23 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
       rrank[R * RS + t] = (t < deg) ? rank[chk_nb(C, R, t)] : (t == deg ? rank[C.n + R] : NONE16);
   }
   __syncwarp();
+#ifdef ALP_PEEL_SPLIT
+  if (F.lane == 0) F.cyc[CY_CUT] += clock64() - tp0;   // diagnostics: peel initialisation
+#endif
+#ifdef ALP_PEEL_BATCH
+  if (C.W <= 32 && RS == 8) peel_picks_batch<1, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (C.W <= 32 && RS == 16) peel_picks_batch<1, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (C.W <= 128 && RS == 8) peel_picks_batch<4, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (C.W <= 128 && RS == 16) peel_picks_batch<4, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else if (RS == 8) peel_picks_batch<0, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+  else peel_picks_batch<0, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
+#else
   if (C.W <= 32 && RS == 8) peel_picks_reg<1, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
   else if (C.W <= 32 && RS == 16) peel_picks_reg<1, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
   else if (C.W <= 128 && RS == 8) peel_picks_reg<4, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
   else if (C.W <= 128 && RS == 16) peel_picks_reg<4, 16>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
   else peel_picks_smem(F, p, order, rrank, RS, cntR, xrR, bm, pos, pcol, prow);
+#endif
 }
 
 // =====================================================================================
@@ -1259,10 +1401,12 @@ __device__ ALP_CALL_BUILD void build_precond(const Frame& F, int p, int& nLb, in
   else if (mts == 3) peel_incremental(F, p, nv);
   else peel_columnwise(F, p);
   long long t2 = clock64();
+#ifndef ALP_PEEL_COUNT
   if (F.lane == 0) {
     F.cyc[CY_SORT] += t1 - t0;
     F.cyc[CY_PEEL] += t2 - t1;
   }
+#endif
   uint16_t* poc = F.S<uint16_t>(L.s_poc);
   const uint16_t* prow = F.S<uint16_t>(L.s_prow);
   const uint16_t* pcol = F.S<uint16_t>(L.s_pcol);
