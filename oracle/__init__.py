@@ -15,6 +15,9 @@ Modules
   lp        Alg. 2 cut search, MALP-A / MALP-B (Alg. 3), plain ALP (Alg. 1),
             augmented form (§IV-B), infeasible primal-dual IPM with a direct
             (Cholesky) step solve, decode outputs and ML certificate.
+  lp_library  Alg. 3 with the LP step (line 13) handed to a library LP solver (scipy HiGHS)
+            instead of the dense IPM — the oracle for config 4 (n = 32,000), where the dense
+            Cholesky IPM takes an hour per frame and ends on its cap.
   precond   Alg. 5 Triangulation Step, Alg. 6 incremental / Alg. 7 column-wise /
             Alg. 8 row-wise greedy MTS, the 3-stage preconditioner apply,
             PCG (Alg. 4).

@@ -367,7 +367,8 @@ def decode_outputs(code, gamma, u, tau_cert, lp_converged=True):
     return hard, obj, g_max, cert
 
 
-def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, record=False):
+def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, record=False,
+                lp_solver=None):
     """Adaptive LP decoding of one frame.
 
     variant "A": MALP-A, Alg. 3.  For every check j (all read u^{k-1}):
@@ -380,6 +381,8 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
     At most alp_max_iter LPs (C-12); a frame that would need more gets ST_ALP_MAXITER, and
     so does a MALP frame whose new pool equals the pool of an LP it already solved (the
     deterministic cycle C-12 describes; detected before solving the repeat).
+    lp_solver: the LP step of line 13 (default: ipm_solve, this module's IPM); oracle/lp_library.py
+    passes a library LP solver with the same call shape (large n, where the dense IPM is too slow).
     """
     P = dict(DEFAULT_PARAMS) if params is None else params
     gamma = np.asarray(gamma, dtype=np.float64)
@@ -428,7 +431,7 @@ def malp_decode(code, gamma, variant: str = "A", params=None, step_solver=None, 
             lp = _augmented_multi(code, alp_rows, gamma)
         else:
             lp = augmented_lp(code, pool, gamma)
-        res = ipm_solve(lp["A"], lp["b"], lp["c"], P, step_solver=step_solver)
+        res = (lp_solver or ipm_solve)(lp["A"], lp["b"], lp["c"], P, step_solver=step_solver)
         lp_solves += 1
         ipm_iters += res["iters"]
         max_p = max(max_p, lp["p"])

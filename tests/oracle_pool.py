@@ -27,9 +27,12 @@ def _init():
 
 
 def _decode_job(job):
-    cfg, snr_idx, frames, variant, llr_scale = job
+    cfg, snr_idx, frames, variant, llr_scale, library = job
     from synth import config_code, config_frames
-    from oracle.lp import malp_decode
+    if library:     # Alg. 3 with the LP step by HiGHS (oracle/lp_library.py): never ends on an IPM cap
+        from oracle.lp_library import malp_decode_library as malp_decode
+    else:
+        from oracle.lp import malp_decode
     code = config_code(cfg)
     fb = config_frames(cfg, snr_idx, frames=frames, code=code) if cfg == 2 else \
         config_frames(cfg, frames=frames, code=code)
@@ -64,10 +67,12 @@ def _pool(n_jobs):
 
 
 def oracle_decode(cfg: int, frames, snr_idx: int = 0, variant: str = "A", llr_scale: float = 1.0,
-                  chunk: int = 2) -> list:
-    """malp_decode on config `cfg` frames (same seeded inputs as the GPU tests), in order."""
+                  chunk: int = 2, library: bool = False) -> list:
+    """malp_decode (library=True: malp_decode_library) on config `cfg` frames (same seeded inputs
+    as the GPU tests), in order."""
     frames = list(frames)
-    jobs = [(cfg, snr_idx, frames[i:i + chunk], variant, llr_scale) for i in range(0, len(frames), chunk)]
+    jobs = [(cfg, snr_idx, frames[i:i + chunk], variant, llr_scale, library)
+            for i in range(0, len(frames), chunk)]
     with _pool(len(jobs)) as ex:
         return [o for part in ex.map(_decode_job, jobs) for o in part]
 

@@ -1,7 +1,10 @@
 """Writes tests/golden/c4_oracle_f<k>.npz: the ORACLE's MALP-A decode of config-4 frames
 (n = 32,000, m = 16,000, 2.2 dB; SURVEY §8(c) c.5 "C4 the first 2 (offline)").  Calls only
 oracle/ and synth/ (never the CUDA path); each frame costs about an hour of CPU (dense
-Cholesky of p ~ 1e4 per Newton step), so it runs offline and its outputs are committed.
+Cholesky of p ~ 1e4 per Newton step).  Result (round 2): frames 0 and 1 both ended on the
+oracle's Newton-step cap (status IPM_MAXITER after 5436 s / 3894 s, > 1e5 C-29 pivot fixes), so
+these outputs cannot gate P1-P3 and are no longer committed; the config-4 parity test uses
+tools/make_c4_golden_library.py (the same Alg. 3 with the LP step solved by HiGHS) instead.
 
   python tools/make_c4_golden.py FRAME [FRAME ...]
 """
