@@ -110,3 +110,28 @@ def test_certificate_rejects_perturbed_library_answer():
         assert not dual_certificate(code, fb.llr[f], u, b["y"], b["masks"])["ok"]
         return
     pytest.skip("no frame needed an LP")
+
+
+def test_e3_largest_lp_of_malp_smaller_than_alp():
+    """The value the paper prints for E3: the largest LP (cut rows) of MALP-A / MALP-B is
+    smaller on average than plain ALP's by 17 % (integral outputs) / 30 % (fractional outputs).
+    Pins Alg. 1 (no removal) against Alg. 3 (removal) in the oracle on 64 frames of an n = 480
+    (3,6) code at 2 dB (the paper's E1 length and SNR); 1000 trials per length are in
+    profiles/r2_e3_largest_lp.json (-14 % / -28 % at n = 480, -17 % / -31 % at n = 1920)."""
+    from synth import awgn_frames
+    code = regular_code(480, 3, 6, seed=3480, girth6=True)
+    fb = awgn_frames(code, 2.0, 4480, 0, range(64), random_codeword=False)
+    big = {v: {0: [], 1: []} for v in ("ALP", "A", "B")}
+    for f in range(fb.F):
+        outs = {v: malp_decode(code, fb.llr[f], v, lp_solver=library_lp_solve) for v in ("ALP", "A", "B")}
+        assert all(o["status"] == 0 for o in outs.values())
+        # Thm 2c (P:279-283): with or without removal the final LP optimum is the same
+        assert abs(outs["A"]["obj"] - outs["ALP"]["obj"]) <= 1e-7 and abs(outs["B"]["obj"] - outs["ALP"]["obj"]) <= 1e-7
+        assert outs["A"]["max_p"] <= outs["ALP"]["max_p"] and outs["A"]["max_p"] <= code.m   # Cor. 3
+        for v, o in outs.items():
+            big[v][outs["ALP"]["cert"]].append(o["max_p"])
+    for v in ("A", "B"):
+        r_int = np.mean(big[v][1]) / np.mean(big["ALP"][1]) - 1.0
+        r_frac = np.mean(big[v][0]) / np.mean(big["ALP"][0]) - 1.0
+        assert -0.25 <= r_int <= -0.08, (v, r_int)
+        assert -0.42 <= r_frac <= -0.18, (v, r_frac)
