@@ -343,7 +343,9 @@ def run_ours(args):
     # dominant (only) kernel: alp_decode_kernel, one launch per step on `stream`
     achieved = pcg_bytes / (t_rank / args.steps) / 1e9
     traffic, traffic_src = None, None
-    try:   # DRAM bytes per frame from the committed ncu --set full capture, scaled to this launch
+    try:   # DRAM bytes per frame from the committed ncu --set full capture (C2), scaled to this launch
+        if args.config != 2:
+            raise OSError("no capture for this config")
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
         traffic = float(tj["dram_bytes_per_frame"]) * F

@@ -52,7 +52,9 @@ struct StepIO {
 
 }  // namespace alp
 
-// The device code twice: shared-memory window (sm) and generic window (gm).
+// The device code three times: shared-memory window (sm), generic window with the graph in
+// global memory (gm; large codes), generic window with the graph staged in shared memory and
+// read by LDS (gs; config 5).
 #define ALP_NS sm
 #define ALP_SM 1
 #include "alp_device.cuh"
@@ -65,6 +67,14 @@ struct StepIO {
 #include "alp_kernels.cuh"
 #undef ALP_NS
 #undef ALP_SM
+#define ALP_NS gs
+#define ALP_SM 0
+#define ALP_GRAPH_SH 1
+#include "alp_device.cuh"
+#include "alp_kernels.cuh"
+#undef ALP_NS
+#undef ALP_SM
+#undef ALP_GRAPH_SH
 
 // =====================================================================================
 // Host side
@@ -111,6 +121,7 @@ DCode make_dcode(const alp_code* c) {
   C.var_chk = c->d_var_chk;
   C.var_slot = c->d_var_slot;
   C.var_deg = c->d_var_deg;
+  C.so_chk_var = C.so_chk_deg = C.so_var_chk = C.so_var_deg = 0;   // set by stage_graph
   return C;
 }
 
@@ -454,6 +465,7 @@ const size_t kCounterBytes = 256;
 // global window for large codes).
 struct Plan {
   bool sm;
+  bool gs = false;
   Layout L;
   GraphSmem G;
   LaunchCfg cfg;
@@ -473,7 +485,8 @@ alp_status make_plan(const alp_code* code, int64_t units, const alp_params* p, b
   if (!want_gm && make_layout_sm(C, pl.L, sm_d2)) {
     // worth it when at least 4 windows fit a CTA (C1, C2; measured: config 5's 92 KB windows run
     // faster in the generic mode, 151 k vs 103 k systems/s)
-    if (4LL * pl.L.smem_bytes + pl.G.bytes <= optin - 1024) {
+    // (sm mode reads the graph from its staged shared copy: G.bytes > 0 is required)
+    if (pl.G.bytes > 0 && 4LL * pl.L.smem_bytes + pl.G.bytes <= optin - 1024) {
       pl.sm = true;
       return step ? plan_launch(sm::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
                   : plan_launch(sm::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
@@ -481,6 +494,10 @@ alp_status make_plan(const alp_code* code, int64_t units, const alp_params* p, b
   }
   pl.sm = false;
   pl.L = make_layout(C, smem_budget_for(p));
+  pl.gs = pl.G.bytes > 0;   // graph staged in shared memory: the kernels that read it by LDS
+  if (pl.gs)
+    return step ? plan_launch(gs::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
+                : plan_launch(gs::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
   return step ? plan_launch(gm::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
               : plan_launch(gm::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
 }
@@ -707,6 +724,9 @@ alp_status alp_decode(const alp_code* code, int64_t n_frames, const double* llr,
   if (pl.sm)
     sm::alp_decode_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
         C, make_params(params), pl.L, pl.G, slots, llr, (long long)n_frames, O, counter);
+  else if (pl.gs)
+    gs::alp_decode_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
+        C, make_params(params), pl.L, pl.G, slots, llr, (long long)n_frames, O, counter);
   else
     gm::alp_decode_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
         C, make_params(params), pl.L, pl.G, slots, llr, (long long)n_frames, O, counter);
@@ -801,6 +821,9 @@ alp_status ipm_step_pcg(const alp_code* code, int64_t n_sys, const uint16_t* mas
   char* slots = (char*)workspace + kCounterBytes;
   if (pl.sm)
     sm::pcg_step_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
+        C, make_params(params), pl.L, pl.G, slots, (long long)n_sys, io, counter);
+  else if (pl.gs)
+    gs::pcg_step_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(
         C, make_params(params), pl.L, pl.G, slots, (long long)n_sys, io, counter);
   else
     gm::pcg_step_kernel<<<pl.cfg.grid, 32 * pl.cfg.wpb, pl.cfg.smem_block, s>>>(

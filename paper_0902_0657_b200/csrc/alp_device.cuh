@@ -69,6 +69,9 @@ struct DCode {
   const uint16_t* __restrict__ var_chk;   // [n][dv] checks of each variable, 0xffff padded
   const uint8_t* __restrict__ var_slot;   // [n][dv] position t of the variable in N(check)
   const uint8_t* __restrict__ var_deg;    // [n]
+  // byte offsets of the staged copies in the CTA's dynamic shared memory (stage_graph; sm mode
+  // forms the graph addresses from the shared-memory symbol itself, so graph reads are LDS)
+  int so_chk_var, so_chk_deg, so_var_chk, so_var_deg;
 };
 
 // Per-CTA shared copy of the Tanner graph (host-computed byte offsets; 0 bytes = stay global).
@@ -80,6 +83,7 @@ struct GraphSmem {
 // DCode whose pointers address that copy (graph reads become shared-memory loads).
 __device__ __forceinline__ void stage_graph(const DCode& C, const GraphSmem& G, char* g, DCode& out) {
   out = C;
+  out.so_chk_var = out.so_chk_deg = out.so_var_chk = out.so_var_deg = 0;
   if (G.bytes == 0) return;
   auto cp = [&](const void* src, int off, int bytes) {
     const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
@@ -95,6 +99,10 @@ __device__ __forceinline__ void stage_graph(const DCode& C, const GraphSmem& G, 
   out.var_chk = reinterpret_cast<const uint16_t*>(g + G.o_var_chk);
   // var_slot stays global: only build_signs reads it, once per LP
   out.var_deg = reinterpret_cast<const uint8_t*>(g + G.o_var_deg);
+  out.so_chk_var = G.o_chk_var;
+  out.so_chk_deg = G.o_chk_deg;
+  out.so_var_chk = G.o_var_chk;
+  out.so_var_deg = G.o_var_deg;
 }
 
 // Byte offsets inside one warp's global slot and shared-memory window (host-computed).
@@ -165,15 +173,6 @@ __device__ __forceinline__ char* rel_ptr(const Layout* L, char* slot, char* sm, 
   return ((L->smask >> k) & 1u) ? sm + L->soff[k] : slot + g;
 }
 
-__device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
-  const unsigned v = C.chk_var[j * C.dc + t];
-  return v == 0xffffu ? -1 : (int)v;
-}
-__device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
-  const unsigned v = C.var_chk[i * C.dv + k];
-  return v == 0xffffu ? -1 : (int)v;
-}
-
 }  // namespace alp
 #endif  // ALP_DEVICE_TYPES
 
@@ -193,8 +192,35 @@ __device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
 #else
 #define ALP_SHA(p) ALP_SH(p)
 #endif   // (an __isGlobal assume broke the NVVM module; generic loads stay)
+// Graph arrays: in the sm and gs instances the graph is always staged (make_plan), and its addresses
+// are formed from the dynamic shared-memory symbol (LDS; a pointer kept in DCode compiles to
+// generic loads).
+#undef ALP_G_CHK_VAR
+#undef ALP_G_CHK_DEG
+#undef ALP_G_VAR_CHK
+#undef ALP_G_VAR_DEG
+#if (ALP_SM || defined(ALP_GRAPH_SH)) && !defined(ALP_GRAPH_GENERIC)
+#define ALP_G_CHK_VAR(C) (reinterpret_cast<const uint16_t*>(alp_dsmem + (C).so_chk_var))
+#define ALP_G_CHK_DEG(C) (reinterpret_cast<const uint8_t*>(alp_dsmem + (C).so_chk_deg))
+#define ALP_G_VAR_CHK(C) (reinterpret_cast<const uint16_t*>(alp_dsmem + (C).so_var_chk))
+#define ALP_G_VAR_DEG(C) (reinterpret_cast<const uint8_t*>(alp_dsmem + (C).so_var_deg))
+#else
+#define ALP_G_CHK_VAR(C) ((C).chk_var)
+#define ALP_G_CHK_DEG(C) ((C).chk_deg)
+#define ALP_G_VAR_CHK(C) ((C).var_chk)
+#define ALP_G_VAR_DEG(C) ((C).var_deg)
+#endif
 namespace alp {
 namespace ALP_NS {
+
+__device__ __forceinline__ int chk_nb(const DCode& C, int j, int t) {
+  const unsigned v = ALP_G_CHK_VAR(C)[j * C.dc + t];
+  return v == 0xffffu ? -1 : (int)v;
+}
+__device__ __forceinline__ int var_ck(const DCode& C, int i, int k) {
+  const unsigned v = ALP_G_VAR_CHK(C)[i * C.dv + k];
+  return v == 0xffffu ? -1 : (int)v;
+}
 
 // Per-frame working set: pointers into the warp's global slot and shared window.
 struct Frame {
@@ -333,7 +359,7 @@ __device__ ALP_HEAVY void build_signs(const Frame& F, bool want_b, int& p_out, i
     uint16_t mk = F.mask[j];
     uint16_t s = 0;
     if (mk & PRESENT) {
-      int deg = C.chk_deg[j];
+      int deg = ALP_G_CHK_DEG(C)[j];
       int nflipV = 0, nflipNotV = 0;
       for (int t = 0; t < deg; ++t) {
         int i = chk_nb(C, j, t);
@@ -357,7 +383,7 @@ __device__ ALP_HEAVY void build_signs(const Frame& F, bool want_b, int& p_out, i
   __syncwarp();
   int nact = 0;
   for (int i = F.lane; i < C.n; i += 32) {
-    int dv = C.var_deg[i];
+    int dv = ALP_G_VAR_DEG(C)[i];
     uint8_t s = 0;
     for (int k = 0; k < dv; ++k) {
       int j = var_ck(C, i, k);
@@ -389,7 +415,7 @@ __device__ ALP_HEAVY bool cut_search(const Frame& F, const Params& P) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   bool changed = false;
   for (int j = F.lane; j < C.m; j += 32) {
-    int deg = C.chk_deg[j];
+    int deg = ALP_G_CHK_DEG(C)[j];
     double uu[DCMAX];
 #pragma unroll
     for (int t = 0; t < DCMAX; ++t) uu[t] = (t < deg) ? F.u[chk_nb(C, j, t)] : 0.0;
@@ -872,7 +898,7 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
     int cn = 0, x = 0;
     if (c < C.n) {
       uint8_t s = F.sgnV_()[c];
-      int dv = C.var_deg[c];
+      int dv = ALP_G_VAR_DEG(C)[c];
       for (int k = 0; k < dv; ++k)
         if ((s >> k) & 1) {
           ++cn;
@@ -888,7 +914,7 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
   }
   for (int R = F.lane; R < C.m; R += 32) {
     if (!(F.sgnC_()[R] & PRESENT)) continue;
-    const int deg = C.chk_deg[R];
+    const int deg = ALP_G_CHK_DEG(C)[R];
     for (int t = 0; t < RS; ++t)
       rrank[R * RS + t] = (t < deg) ? rank[chk_nb(C, R, t)] : (t == deg ? rank[C.n + R] : NONE16);
   }
@@ -972,9 +998,9 @@ __device__ __noinline__ void peel_rowwise_t(const Frame& F, int p, int nv) {
   for (int j = F.lane; j < m; j += 32) {
     int dg = 0, x = 0;
     if (sgnC[j] & PRESENT) {
-      const int deg = C.chk_deg[j];
+      const int deg = ALP_G_CHK_DEG(C)[j];
       for (int t = 0; t < deg; ++t) {
-        const int c = C.chk_var[j * C.dc + t];
+        const int c = ALP_G_CHK_VAR(C)[j * C.dc + t];
         ++dg;
         x ^= c;
       }
@@ -1030,7 +1056,7 @@ __device__ __noinline__ void peel_rowwise_t(const Frame& F, int p, int nv) {
     // remove column c from A~: its rows lose one live column
     int r = -1;
     if (c < n) {
-      if (F.lane < DVMAX && ((sgnV[c] >> F.lane) & 1)) r = C.var_chk[c * C.dv + F.lane];
+      if (F.lane < DVMAX && ((sgnV[c] >> F.lane) & 1)) r = ALP_G_VAR_CHK(C)[c * C.dv + F.lane];
     } else if (F.lane == 0) {
       r = c - n;
     }
@@ -1132,9 +1158,9 @@ __device__ __noinline__ int tri_step(const Frame& F, const uint8_t* inM, uint8_t
   for (int j = F.lane; j < m; j += 32) {
     int dg = 0, x = 0;
     if (sgnC[j] & PRESENT) {
-      const int deg = C.chk_deg[j];
+      const int deg = ALP_G_CHK_DEG(C)[j];
       for (int t = 0; t < deg; ++t) {
-        const int c = C.chk_var[j * C.dc + t];
+        const int c = ALP_G_CHK_VAR(C)[j * C.dc + t];
         if (inM[c]) {
           ++dg;
           x ^= c;
@@ -1171,7 +1197,7 @@ __device__ __noinline__ int tri_step(const Frame& F, const uint8_t* inM, uint8_t
     // line 8: zero column c (its rows, the picked row j among them, lose it)
     int r = -1;
     if (c < n) {
-      if (F.lane < DVMAX && ((sgnV[c] >> F.lane) & 1)) r = C.var_chk[c * C.dv + F.lane];
+      if (F.lane < DVMAX && ((sgnV[c] >> F.lane) & 1)) r = ALP_G_VAR_CHK(C)[c * C.dv + F.lane];
     } else if (F.lane == 0) {
       r = c - n;
     }
@@ -1238,14 +1264,14 @@ template <int DCT>
 __device__ __forceinline__ void back_deps(const Frame& F, int R, int (&deps)[DCT]) {
   const DCode C = *F.C;   // register copy: graph pointers / dims not re-read from shared memory
   const uint16_t* poc = F.S<uint16_t>(F.L->s_poc);
-  const int deg = C.chk_deg[R];
+  const int deg = ALP_G_CHK_DEG(C)[R];
   const uint16_t s = F.sgnC_()[R];
   const int pc = F.S<uint16_t>(F.L->s_pcol)[R];
 #pragma unroll
   for (int t = 0; t < DCT; ++t) {
     int v = DEP_NONE;
     if (t < deg) {
-      const int c = C.chk_var[R * C.dc + t];
+      const int c = ALP_G_CHK_VAR(C)[R * C.dc + t];
       const uint16_t rr = (c == pc) ? NONE16 : poc[c];
       if (rr != NONE16) v = (int)rr | (int)(((unsigned)(s >> t) & 1u) << 31);
     }
@@ -1260,7 +1286,7 @@ __device__ __forceinline__ void fwd_deps(const Frame& F, int R, int (&deps)[DVMA
   for (int k = 0; k < DVMAX; ++k) {
     int v = DEP_NONE;
     if ((s >> k) & 1) {
-      const int j = C.var_chk[c * C.dv + k];
+      const int j = ALP_G_VAR_CHK(C)[c * C.dv + k];
       if (j != R) v = j | (int)(((unsigned)(s >> (4 + k)) & 1u) << 31);
     }
     deps[k] = v;
@@ -1272,7 +1298,7 @@ __device__ __forceinline__ int diag_neg(const Frame& F, int R) {
   int c = F.S<uint16_t>(F.L->s_pcol)[R];
   if (c >= C.n) return 0;
   uint8_t s = F.sgnV_()[c];
-  int dv = C.var_deg[c];
+  int dv = ALP_G_VAR_DEG(C)[c];
   for (int k = 0; k < dv; ++k)
     if (var_ck(C, c, k) == R) return (s >> (4 + k)) & 1;
   return 0;
@@ -1700,7 +1726,7 @@ __device__ ALP_PCGPART double spmv_vars(const Frame& F, const DCode& C) {
   double* __restrict__ tS = F.fz_();
   const uint8_t* __restrict__ sgnV = F.sgnV_();
   const uint16_t* __restrict__ sgnC = F.sgnC_();
-  const uint16_t* __restrict__ var_chk = C.var_chk;
+  const uint16_t* __restrict__ var_chk = ALP_G_VAR_CHK(C);
   const double* __restrict__ d2 = F.d2;
   const int n = C.n;
   double hl = 0.0;
@@ -1791,8 +1817,8 @@ __device__ ALP_PCGPART double spmv_checks(const Frame& F, const DCode& C, double
   const double* __restrict__ hS = F.h_();
   const double* __restrict__ tS = F.fz_();
   const uint16_t* __restrict__ sgnC = F.sgnC_();
-  const uint16_t* __restrict__ chk_var = C.chk_var;
-  const uint8_t* __restrict__ chk_deg = C.chk_deg;
+  const uint16_t* __restrict__ chk_var = ALP_G_CHK_VAR(C);
+  const uint8_t* __restrict__ chk_deg = ALP_G_CHK_DEG(C);
   const double* __restrict__ d2s_ = F.d2 + C.n;
   const double* __restrict__ W = F.w;
   double* __restrict__ rS = F.r_();
@@ -1923,12 +1949,12 @@ __device__ __noinline__ double residual_dd(const Frame& F, double* rS) {
     double r = 0.0;
     if (sc & PRESENT) {
       DD l = dd_mul(DD{F.dy_()[j], 0.0}, F.d2[C.n + j]);
-      const int deg = C.chk_deg[j];
+      const int deg = ALP_G_CHK_DEG(C)[j];
       for (int t = 0; t < deg; ++t) {
         const int i = chk_nb(C, j, t);
         const uint8_t sv = F.sgnV_()[i];
         DD ti{0.0, 0.0};
-        for (int k = 0; k < C.var_deg[i]; ++k) {
+        for (int k = 0; k < ALP_G_VAR_DEG(C)[i]; ++k) {
           if (!((sv >> k) & 1)) continue;
           const double h = F.dy_()[var_ck(C, i, k)];
           ti = dd_add(ti, ((sv >> (4 + k)) & 1) ? -h : h);

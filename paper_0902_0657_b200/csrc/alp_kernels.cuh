@@ -31,13 +31,13 @@ __device__ __forceinline__ void ipm_rows_residual(const DCode& C, int lane, cons
     for (int u = 0; u < UBR; ++u) {
       const int j = min(j0 + 32 * u, m - 1);
       sc[u] = (j0 + 32 * u < m) ? SC[j] : (uint16_t)0;
-      deg[u] = C.chk_deg[j];
+      deg[u] = ALP_G_CHK_DEG(C)[j];
       bj[u] = B[j];
       xsl[u] = X[n + j];
       yj[u] = Y[j];
       zsl[u] = Z[n + j];
 #pragma unroll
-      for (int t = 0; t < DCT; ++t) xs[u][t] = (t < deg[u]) ? X[C.chk_var[j * C.dc + t]] : 0.0;
+      for (int t = 0; t < DCT; ++t) xs[u][t] = (t < deg[u]) ? X[ALP_G_CHK_VAR(C)[j * C.dc + t]] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < UBR; ++u) {
@@ -72,11 +72,11 @@ __device__ __forceinline__ void ipm_rows_w(const DCode& C, int lane, const uint1
     for (int u = 0; u < UBR; ++u) {
       const int j = min(j0 + 32 * u, m - 1);
       sc[u] = (j0 + 32 * u < m) ? SC[j] : (uint16_t)0;
-      deg[u] = C.chk_deg[j];
+      deg[u] = ALP_G_CHK_DEG(C)[j];
       wj[u] = W[j];
       vsl[u] = V[n + j];
 #pragma unroll
-      for (int t = 0; t < DCT; ++t) vs[u][t] = (t < deg[u]) ? V[C.chk_var[j * C.dc + t]] : 0.0;
+      for (int t = 0; t < DCT; ++t) vs[u][t] = (t < deg[u]) ? V[ALP_G_CHK_VAR(C)[j * C.dc + t]] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < UBR; ++u) {
@@ -105,11 +105,11 @@ __device__ __forceinline__ void ipm_rows_rho(const DCode& C, int lane, const uin
     for (int u = 0; u < UBR; ++u) {
       const int j = min(j0 + 32 * u, m - 1);
       sc[u] = (j0 + 32 * u < m) ? SC[j] : (uint16_t)0;
-      const int deg = (sc[u] & PRESENT) ? (int)C.chk_deg[j] : 0;
+      const int deg = (sc[u] & PRESENT) ? (int)ALP_G_CHK_DEG(C)[j] : 0;
       rb[u] = RBv[j];
       vsl[u] = V[n + j];
 #pragma unroll
-      for (int t = 0; t < DCT; ++t) vs[u][t] = (t < deg) ? V[C.chk_var[j * C.dc + t]] : 0.0;
+      for (int t = 0; t < DCT; ++t) vs[u][t] = (t < deg) ? V[ALP_G_CHK_VAR(C)[j * C.dc + t]] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < UBR; ++u) {
@@ -196,7 +196,7 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
         zi[u] = Z[i];
         xi[u] = X[i];
 #pragma unroll
-        for (int k = 0; k < DVMAX; ++k) ys[u][k] = Y[min((int)C.var_chk[i * C.dv + k], m - 1)];
+        for (int k = 0; k < DVMAX; ++k) ys[u][k] = Y[min((int)ALP_G_VAR_CHK(C)[i * C.dv + k], m - 1)];
       }
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
@@ -304,7 +304,7 @@ __device__ ALP_CALL_IPM IpmOut ipm_solve(const Frame& F, const Params& P, const 
         vi[u] = V[i];
         rci[u] = RCv[i];
 #pragma unroll
-        for (int k = 0; k < DVMAX; ++k) dys[u][k] = ((sv[u] >> k) & 1) ? DY[C.var_chk[i * C.dv + k]] : 0.0;
+        for (int k = 0; k < DVMAX; ++k) dys[u][k] = ((sv[u] >> k) & 1) ? DY[ALP_G_VAR_CHK(C)[i * C.dv + k]] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
@@ -563,7 +563,7 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   }
   bool parity_bad = false;
   for (int j = lane; j < m; j += 32) {
-    int deg = C.chk_deg[j];
+    int deg = ALP_G_CHK_DEG(C)[j];
     int par = 0;
     for (int t = 0; t < deg; ++t) par ^= (F.u[chk_nb(C, j, t)] > 0.5) ? 1 : 0;
     parity_bad |= (par != 0);
