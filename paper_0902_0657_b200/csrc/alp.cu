@@ -339,7 +339,11 @@ GraphSmem make_graph_smem(const DCode& C) {
   G.o_var_slot = 0;   // not staged (build_signs reads it from global memory once per LP)
   G.o_var_deg = a(C.n);
   G.bytes = (int)al(o, 128);
-  if (G.bytes > 48 * 1024) G = GraphSmem{0, 0, 0, 0, 0, 0};   // large codes: graph stays global
+  // large codes: graph stays global (ALP_GRAPH_MAX_KB overrides the 72 KB limit for tuning runs;
+  // make_plan drops a staged graph above 48 KB when it would cost a resident frame)
+  int max_kb = 72;
+  if (const char* ev = getenv("ALP_GRAPH_MAX_KB")) max_kb = atoi(ev);
+  if (G.bytes > max_kb * 1024) G = GraphSmem{0, 0, 0, 0, 0, 0};
   return G;
 }
 
@@ -494,7 +498,16 @@ alp_status make_plan(const alp_code* code, int64_t units, const alp_params* p, b
   }
   pl.sm = false;
   pl.L = make_layout(C, smem_budget_for(p));
-  pl.gs = pl.G.bytes > 0;   // graph staged in shared memory: the kernels that read it by LDS
+  // gs kernels: graph staged in shared memory and read by LDS (the window keeps generic pointers:
+  // an LDS-addressed window measured 8 % slower on config 5, profiles/r2_ab_g31.log).  A graph
+  // above 48 KB is staged only if it costs no resident frame (config 3: 2 x 78 KB windows + 69 KB).
+  if (pl.G.bytes > 48 * 1024) {
+    const int want = (p && p->warps_per_block > 0) ? p->warps_per_block : 4;
+    int w0 = want;
+    while (w0 > 1 && (long long)w0 * pl.L.smem_bytes > optin - 1024) --w0;
+    if (pl.L.win_global || (long long)w0 * pl.L.smem_bytes + pl.G.bytes > optin - 1024) pl.G = GraphSmem{0, 0, 0, 0, 0, 0};
+  }
+  pl.gs = pl.G.bytes > 0;
   if (pl.gs)
     return step ? plan_launch(gs::pcg_step_kernel, pl.L, pl.G.bytes, units, p, pl.cfg)
                 : plan_launch(gs::alp_decode_kernel, pl.L, pl.G.bytes, units, p, pl.cfg);
