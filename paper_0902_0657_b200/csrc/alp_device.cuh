@@ -244,6 +244,10 @@ struct Frame {
   // loads).  smo = the frame window's byte offset in dynamic shared memory.
   unsigned smo;
   unsigned o_sgnC, o_sgnV, o_dy, o_dinvF, o_recB, o_recF, o_offB, o_offF;
+#ifdef ALP_CACHE_OFFS
+  unsigned o_h, o_r, o_fz;   // PCG vectors: offsets kept in registers (L lives in shared memory
+                             // behind a generic pointer, a slow load per accessor call)
+#endif
   template <class T>
   __device__ __forceinline__ T* S(int off) const { return reinterpret_cast<T*>(alp_dsmem + smo + off); }
   template <class T>
@@ -258,6 +262,8 @@ struct Frame {
   __device__ __forceinline__ double* dy_() const { return W_<double>(o_dy); }
 #ifdef ALP_SM_R_SLOT
   __device__ __forceinline__ double* r_() const { return r; }     // slot (tuning variant)
+#elif defined(ALP_CACHE_OFFS)
+  __device__ __forceinline__ double* r_() const { return W_<double>(o_r); }
 #else
   __device__ __forceinline__ double* r_() const { return S<double>(L->s_r); }
 #endif
@@ -275,8 +281,13 @@ struct Frame {
   __device__ __forceinline__ double* r_() const { return S<double>(L->s_r); }
 #endif
   __device__ __forceinline__ uint16_t* pcolR_() const { return pcolR; }
+#if ALP_SM && defined(ALP_CACHE_OFFS)
+  __device__ __forceinline__ double* h_() const { return W_<double>(o_h); }
+  __device__ __forceinline__ double* fz_() const { return W_<double>(o_fz); }
+#else
   __device__ __forceinline__ double* h_() const { return S<double>(L->s_h); }
   __device__ __forceinline__ double* fz_() const { return S<double>(L->s_fz); }
+#endif
 };
 
 __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layout* L, char* slot,
@@ -320,6 +331,11 @@ __device__ __forceinline__ void frame_bind(Frame& F, const DCode* C, const Layou
   F.o_recF = L->soff[RL_RECF];
   F.o_offB = L->soff[RL_OFFB];
   F.o_offF = L->soff[RL_OFFF];
+#ifdef ALP_CACHE_OFFS
+  F.o_h = L->s_h;
+  F.o_r = L->s_r;
+  F.o_fz = L->s_fz;
+#endif
   F.sgnC = F.sgnC_();
   F.sgnV = F.sgnV_();
   F.dy = F.dy_();
