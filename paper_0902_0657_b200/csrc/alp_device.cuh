@@ -40,6 +40,14 @@
 namespace alp {
 
 extern __shared__ __align__(16) char alp_dsmem[];   // the kernels' dynamic shared memory
+#ifdef ALP_CYC_STATIC
+// phase clocks as a file-scope static shared array: ticks compile to LDS/STS at a fixed address
+// (through a generic pointer kept in the Frame each tick is a generic load + store to shared memory)
+__shared__ long long alp_cyc_sh[8][8];
+#define ALP_CYC(F) (alp_cyc_sh[threadIdx.x >> 5])
+#else
+#define ALP_CYC(F) ((F).cyc)
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint16_t PRESENT = 0x8000u;
@@ -161,7 +169,7 @@ enum { CY_CUT = 0, CY_IPM = 1, CY_BUILD = 2, CY_SPMV = 3, CY_SWEEP = 4, CY_PCG =
 #define ALP_TICK(F, ph, t)                          \
   do {                                              \
     long long now_ = clock64();                     \
-    if ((F).lane == 0) (F).cyc[ph] += now_ - (t);   \
+    if ((F).lane == 0) ALP_CYC(F)[ph] += now_ - (t);   \
     (t) = now_;                                     \
   } while (0)
 
@@ -838,8 +846,8 @@ __device__ __forceinline__ void peel_picks_batch(const Frame& F, int p, const ui
     k += nb;
 #ifdef ALP_PEEL_COUNT
     if (F.lane == 0) {   // diagnostics: batches in the sort clock, picks in the peel clock
-      F.cyc[CY_SORT] += 1;
-      F.cyc[CY_PEEL] += nb;
+      ALP_CYC(F)[CY_SORT] += 1;
+      ALP_CYC(F)[CY_PEEL] += nb;
     }
 #endif
   }
@@ -936,7 +944,7 @@ __device__ ALP_HEAVY void peel_columnwise(const Frame& F, int p) {
   }
   __syncwarp();
 #ifdef ALP_PEEL_SPLIT
-  if (F.lane == 0) F.cyc[CY_CUT] += clock64() - tp0;   // diagnostics: peel initialisation
+  if (F.lane == 0) ALP_CYC(F)[CY_CUT] += clock64() - tp0;   // diagnostics: peel initialisation
 #endif
 #ifdef ALP_PEEL_BATCH
   if (C.W <= 32 && RS == 8) peel_picks_batch<1, 8>(F, p, order, rrank, cntR, xrR, bm, pos, pcol, prow);
@@ -1445,8 +1453,8 @@ __device__ ALP_CALL_BUILD void build_precond(const Frame& F, int p, int& nLb, in
   long long t2 = clock64();
 #ifndef ALP_PEEL_COUNT
   if (F.lane == 0) {
-    F.cyc[CY_SORT] += t1 - t0;
-    F.cyc[CY_PEEL] += t2 - t1;
+    ALP_CYC(F)[CY_SORT] += t1 - t0;
+    ALP_CYC(F)[CY_PEEL] += t2 - t1;
   }
 #endif
   uint16_t* poc = F.S<uint16_t>(L.s_poc);

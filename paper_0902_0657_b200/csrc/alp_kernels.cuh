@@ -488,7 +488,7 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
   double max_rec = 0.0, max_true = 0.0;
   bool last_lp_bad = false;   // the last solved LP did not converge (IPM cap / non-finite)
   double pcg_bytes = 0.0;
-  if (lane < 8) F.cyc[lane] = 0;
+  if (lane < 8) ALP_CYC(F)[lane] = 0;
   __syncwarp();
   long long tk = clock64();
   for (int k = 0;; ++k) {
@@ -594,14 +594,14 @@ __device__ void decode_frame(Frame& F, const Params& P, const double* g, long lo
       st.max_true_relres = max_true;
       st.g_max = gm;
       st.pcg_bytes = pcg_bytes;
-      st.cyc_cut = F.cyc[CY_CUT];
-      st.cyc_ipm = F.cyc[CY_IPM];
-      st.cyc_build = F.cyc[CY_BUILD];
-      st.cyc_spmv = F.cyc[CY_SPMV];
-      st.cyc_sweep = F.cyc[CY_SWEEP];
-      st.cyc_pcg_other = F.cyc[CY_PCG];
-      st.cyc_sort = F.cyc[CY_SORT];
-      st.cyc_peel = F.cyc[CY_PEEL];
+      st.cyc_cut = ALP_CYC(F)[CY_CUT];
+      st.cyc_ipm = ALP_CYC(F)[CY_IPM];
+      st.cyc_build = ALP_CYC(F)[CY_BUILD];
+      st.cyc_spmv = ALP_CYC(F)[CY_SPMV];
+      st.cyc_sweep = ALP_CYC(F)[CY_SWEEP];
+      st.cyc_pcg_other = ALP_CYC(F)[CY_PCG];
+      st.cyc_sort = ALP_CYC(F)[CY_SORT];
+      st.cyc_peel = ALP_CYC(F)[CY_PEEL];
       O.stats[f] = st;
     }
   }
@@ -629,8 +629,10 @@ __global__ void __launch_bounds__(256, ALP_MINB) alp_decode_kernel(DCode C, Para
   Frame F;
   char* slot = slots + gw * L.slot_bytes;
   frame_bind(F, &sC, &sL, slot, L.win_global ? slot + L.g_win : smem + G.bytes + warp * L.smem_bytes, lane);
+#ifndef ALP_CYC_STATIC
   __shared__ long long s_cyc[8][8];   // phase clocks in shared memory (a global RMW per tick
   F.cyc = s_cyc[warp];                // would stall the warp on an L2 round trip)
+#endif
   while (true) {
     long long f = 0;
     if (lane == 0) f = (long long)atomicAdd(counter, 1ull);   // 64-bit: no wrap at any n_frames
