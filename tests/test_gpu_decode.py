@@ -267,7 +267,8 @@ def test_certificate_needs_converged_lp():
 @pytest.mark.slow
 def test_config2_full_batch_certified():
     """16,384 frames at 3.0 dB (the bench workload, same launch configuration): P6 on every
-    frame that finished; completion and P1-P3 on a 64-frame oracle sample spread over the batch."""
+    frame that finished; completion and P1-P3 on a 64-frame oracle sample spread over the batch,
+    P1-P3 on 2,048 frames against the library-LP oracle."""
     code = config_code(2)
     fb = config_frames(2, 2)
     g = gpu_decode(code, fb.llr)
@@ -276,6 +277,14 @@ def test_config2_full_batch_certified():
     sample = np.random.default_rng(1).choice(fb.F, 64, replace=False)
     orc = oracle_decode(2, sample, snr_idx=2)
     parity("C2_full_sample", code, fb.llr, g, orc, sample)
+    # every 8th frame of the batch (2,048 frames) against Alg. 3 with the LP step by HiGHS
+    # (oracle/lp_library.py; ~0.3 s per frame per core)
+    wide = list(range(0, fb.F, 8))
+    orl = oracle_decode(2, wide, snr_idx=2, library=True, chunk=16)
+    for o in orl:
+        o["ipm_iters"] = -1
+    rep = parity("C2_full_library_2048", code, fb.llr, g, orl, wide, completion=False)
+    assert rep["compared"] >= 0.99 * len(wide), rep
 
 
 def test_config1_plain_cg_decode():
