@@ -210,6 +210,15 @@ def test_config3_sample():
     orc = oracle_decode(3, range(128))
     parity("C3", code, fb.llr, g, orc)
     assert_certified(code, fb.llr, g)
+    # a wider sample (the first 1,024 frames) against the library-LP oracle (oracle/lp_library.py)
+    fw = config_frames(3, frames=range(1024), code=code)
+    gw = gpu_decode(code, fw.llr)
+    orl = oracle_decode(3, range(1024), library=True, chunk=16)
+    for o in orl:
+        o["ipm_iters"] = -1
+    rep = parity("C3_library_1024", code, fw.llr, gw, orl, completion=False)
+    assert rep["compared"] >= 0.98 * 1024, rep
+    assert_certified(code, fw.llr, gw)
 
 
 @pytest.mark.parametrize("F", [1, 37])
